@@ -1,0 +1,216 @@
+"""CPU oracle for the robust validity of linear hexahedra (section 6).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+the ``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import
+this package.  The product path (``paper_1706_01613_b200``) never imports or
+calls it, and the two share no code: see ``oracle.c`` for what is computed and
+DESIGN.md for the readings of the paper it follows.
+
+This module is ctypes marshalling only; every step of the algorithm runs in
+``liboracle.so`` (plain C, built by :func:`build`).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+SRC = os.path.join(HERE, "oracle.c")
+
+INVALID, VALID, UNDETERMINED, NONFINITE = 0, 1, 2, 3
+FLAG_SUBDIVIDED = 4
+MAX_DEPTH = 20
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O2 -ffp-contract=off, OpenMP)."""
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
+            os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "oracle.h"))):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-Wall",
+               "-shared", "-fPIC", SRC, "-o", LIB_PATH, "-lm"]
+        subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+class OracleResult(ctypes.Structure):
+    _fields_ = [
+        ("verdict", ctypes.c_int),
+        ("subdivided", ctypes.c_int),
+        ("flags", ctypes.c_int),
+        ("exact_used", ctypes.c_int),
+        ("near_boundary", ctypes.c_int),
+        ("max_depth", ctypes.c_int),
+        ("nodes", ctypes.c_int64),
+        ("margin_ratio", ctypes.c_double),
+        ("E", ctypes.c_double),
+        ("c", ctypes.c_double * 27),
+        ("b", ctypes.c_double * 27),
+        ("witness", ctypes.c_double * 3),
+        ("witness_value", ctypes.c_double),
+    ]
+
+    def as_dict(self):
+        return {
+            "verdict": self.verdict, "subdivided": self.subdivided, "flags": self.flags,
+            "exact_used": self.exact_used, "near_boundary": self.near_boundary,
+            "max_depth": self.max_depth, "nodes": self.nodes,
+            "margin_ratio": self.margin_ratio, "E": self.E,
+            "c": np.array(self.c[:]), "b": np.array(self.b[:]),
+            "witness": np.array(self.witness[:]), "witness_value": self.witness_value,
+        }
+
+
+_lib = None
+_D = ctypes.POINTER(ctypes.c_double)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(LIB_PATH)
+        L.oracle_check_hex.argtypes = [_D, ctypes.POINTER(OracleResult)]
+        L.oracle_check_hex.restype = ctypes.c_int
+        L.oracle_check_soa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        L.oracle_check_soa.restype = None
+        L.oracle_check_indexed.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_int]
+        L.oracle_check_indexed.restype = None
+        L.oracle_detj.argtypes = [_D, _D]
+        L.oracle_detj.restype = ctypes.c_double
+        L.oracle_samples27.argtypes = [_D, _D]
+        L.oracle_bezier_from_samples.argtypes = [_D, _D]
+        L.oracle_tb_matrix.argtypes = [_D]
+        L.oracle_bezier_eval.argtypes = [_D, _D]
+        L.oracle_bezier_eval.restype = ctypes.c_double
+        L.oracle_subdivide.argtypes = [_D, ctypes.c_int, _D]
+        L.oracle_exact_sign.argtypes = [_D, ctypes.c_int]
+        L.oracle_exact_sign.restype = ctypes.c_int
+        L.oracle_node_xi.argtypes = [ctypes.c_int, _D]
+        L.oracle_classify_coeffs.argtypes = [_D, ctypes.c_double, ctypes.POINTER(OracleResult)]
+        L.oracle_classify_coeffs.restype = ctypes.c_int
+        L.oracle_num_threads.argtypes = [ctypes.c_int]
+        L.oracle_num_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_D)
+
+
+def _hex(X) -> np.ndarray:
+    X = np.ascontiguousarray(np.asarray(X, dtype=np.float64).reshape(8, 3))
+    return X
+
+
+def check_hex(X) -> dict:
+    """Run the whole algorithm on one hex (8x3 nodes in Fig. 3 order)."""
+    X = _hex(X)
+    r = OracleResult()
+    lib().oracle_check_hex(_dptr(X), ctypes.byref(r))
+    return r.as_dict()
+
+
+def detj(X, xi) -> float:
+    X = _hex(X)
+    xi = np.ascontiguousarray(np.asarray(xi, dtype=np.float64))
+    return lib().oracle_detj(_dptr(X), _dptr(xi))
+
+
+def samples27(X) -> np.ndarray:
+    X = _hex(X)
+    c = np.zeros(27)
+    lib().oracle_samples27(_dptr(X), _dptr(c))
+    return c
+
+
+def bezier_from_samples(c) -> np.ndarray:
+    c = np.ascontiguousarray(np.asarray(c, dtype=np.float64))
+    b = np.zeros(27)
+    lib().oracle_bezier_from_samples(_dptr(c), _dptr(b))
+    return b
+
+
+def tb_matrix() -> np.ndarray:
+    T = np.zeros((27, 27))
+    lib().oracle_tb_matrix(_dptr(T))
+    return T
+
+
+def bezier_eval(b, xi) -> float:
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    xi = np.ascontiguousarray(np.asarray(xi, dtype=np.float64))
+    return lib().oracle_bezier_eval(_dptr(b), _dptr(xi))
+
+
+def subdivide(b, child: int) -> np.ndarray:
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    out = np.zeros(27)
+    lib().oracle_subdivide(_dptr(b), int(child), _dptr(out))
+    return out
+
+
+def exact_sign(X, sigma: int) -> int:
+    X = _hex(X)
+    return lib().oracle_exact_sign(_dptr(X), int(sigma))
+
+
+def node_xi(sigma: int) -> np.ndarray:
+    xi = np.zeros(3)
+    lib().oracle_node_xi(int(sigma), _dptr(xi))
+    return xi
+
+
+def classify_coeffs(b, E: float = 1.0) -> dict:
+    """Steps 4-5 of the algorithm on an arbitrary 27-coefficient vector."""
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    r = OracleResult()
+    lib().oracle_classify_coeffs(_dptr(b), float(E), ctypes.byref(r))
+    return r.as_dict()
+
+
+def num_threads(nthreads: int = 0) -> int:
+    return lib().oracle_num_threads(int(nthreads))
+
+
+def check_soa(coords: np.ndarray, want_coeffs: bool = False, nthreads: int = 0):
+    """Batch over a (24, n) SoA array.  Returns dict of flags / near / nodes / exact (/ coeffs)."""
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    n = coords.shape[1]
+    flags = np.zeros(n, np.uint8)
+    near = np.zeros(n, np.uint8)
+    nodes = np.zeros(n, np.int64)
+    exact = np.zeros(n, np.uint8)
+    coeffs = np.zeros((27, n)) if want_coeffs else None
+    lib().oracle_check_soa(coords.ctypes.data, n, flags.ctypes.data,
+                           coeffs.ctypes.data if coeffs is not None else None,
+                           near.ctypes.data, nodes.ctypes.data, exact.ctypes.data, int(nthreads))
+    out = {"flags": flags, "near": near, "nodes": nodes, "exact": exact}
+    if coeffs is not None:
+        out["coeffs"] = coeffs
+    return out
+
+
+def check_indexed(vertices: np.ndarray, hex_idx: np.ndarray, want_coeffs: bool = False, nthreads: int = 0):
+    vertices = np.ascontiguousarray(vertices, dtype=np.float64)
+    hex_idx = np.ascontiguousarray(hex_idx, dtype=np.int32)
+    n = hex_idx.shape[0]
+    flags = np.zeros(n, np.uint8)
+    near = np.zeros(n, np.uint8)
+    nodes = np.zeros(n, np.int64)
+    exact = np.zeros(n, np.uint8)
+    coeffs = np.zeros((27, n)) if want_coeffs else None
+    lib().oracle_check_indexed(vertices.ctypes.data, hex_idx.ctypes.data, n, flags.ctypes.data,
+                               coeffs.ctypes.data if coeffs is not None else None,
+                               near.ctypes.data, nodes.ctypes.data, exact.ctypes.data, int(nthreads))
+    out = {"flags": flags, "near": near, "nodes": nodes, "exact": exact}
+    if coeffs is not None:
+        out["coeffs"] = coeffs
+    return out

@@ -1,0 +1,402 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (-m "not gpu").
+
+Each test names the passage it checks.  None of them compares the oracle with
+itself: the references are exact rational matrices built from the Bernstein
+definition, an independent shape-function evaluation of det J, closed forms,
+the paper's printed examples, brute-force sampling and Python exact rationals.
+"""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import hexgen
+import oracle
+from tests import pins
+
+U = pins.KAPPA.astype(np.float64)
+
+
+# --------------------------------------------------------------------------
+# constants: Table 1, Table 2, Table 3
+# --------------------------------------------------------------------------
+
+def test_table1_is_inverse_of_bernstein_collocation():
+    """T_b = A^-1 with A_{sigma tau} = B_tau(xi_sigma) (Table 1)."""
+    Ainv = pins.invert_exact(pins.collocation_matrix_exact())
+    T = oracle.tb_matrix()
+    for s in range(27):
+        for t in range(27):
+            assert Fraction(float(T[s, t])) == Ainv[s][t], (s, t)
+
+
+def test_table1_rows_sum_to_one():
+    """Constant functions have constant Bezier coefficients."""
+    T = oracle.tb_matrix()
+    assert np.all(T.sum(axis=1) == 1.0)
+
+
+def test_table3_equals_D_times_Tsub_with_corrected_table2():
+    """Table 3 = D * T_sub; Table 2 as printed has the opposite sign (reading G1)."""
+    Tb = pins.invert_exact(pins.collocation_matrix_exact())
+    Tsub = [row[:20] for row in Tb[:20]]
+    printed = pins.table2_printed_exact()
+    # printed rows sum to -1, which cannot preserve constants
+    assert all(sum(r) == -1 for r in printed)
+    corrected = [[-v for v in r] for r in printed]
+    D = [[Fraction(int(i == j)) for j in range(20)] for i in range(20)] + corrected
+    DT = [[sum(D[i][k] * Tsub[k][j] for k in range(20)) for j in range(20)] for i in range(27)]
+    T3 = pins.table3_exact()
+    assert DT == T3
+    # and with the printed sign the product does not reproduce Table 3
+    Dp = [[Fraction(int(i == j)) for j in range(20)] for i in range(20)] + printed
+    DTp = [[sum(Dp[i][k] * Tsub[k][j] for k in range(20)) for j in range(20)] for i in range(27)]
+    assert DTp != T3
+
+
+def test_oracle_coefficients_match_table3_route():
+    """b = T_b c_27 (oracle) equals T-tilde c_20 (Table 3) on random hexes (Cor. 1)."""
+    T3 = np.array([[float(v) for v in r] for r in pins.table3_exact()])
+    for X in pins.random_hexes(300, 0.45, 1):
+        r = oracle.check_hex(X)
+        b3 = T3 @ r["c"][:20]
+        scale = np.max(np.abs(r["b"]))
+        assert np.max(np.abs(b3 - r["b"])) <= 1e-13 * scale
+
+
+def test_corollary1_seven_monomials_vanish():
+    """m_220 = m_202 = m_022 = m_221 = m_212 = m_122 = m_222 = 0 (Cor. 1)."""
+    t = np.array([0.0, 0.5, 1.0])
+    V1 = np.vander(t, 3, increasing=True)            # 1D Vandermonde on {0,1/2,1}
+    Vi = np.linalg.inv(V1)
+    for X in pins.random_hexes(200, 0.45, 2):
+        c = oracle.samples27(X)
+        C = np.zeros((3, 3, 3))
+        for s in range(27):
+            i, j, k = pins.XI2[s]
+            C[i, j, k] = c[s]
+        M = np.einsum("ai,bj,ck,ijk->abc", Vi, Vi, Vi, C)   # monomial coefficients m_abc
+        scale = np.max(np.abs(M))
+        for (a, b, cc) in [(2, 2, 0), (2, 0, 2), (0, 2, 2), (2, 2, 1), (2, 1, 2), (1, 2, 2), (2, 2, 2)]:
+            assert abs(M[a, b, cc]) <= 1e-12 * scale
+
+
+# --------------------------------------------------------------------------
+# samples and the Bezier expansion
+# --------------------------------------------------------------------------
+
+def test_samples_are_detj_at_nodes():
+    """c_sigma = det J(xi_sigma), vs an independent shape-function evaluation."""
+    nodes = pins.XI2 / 2.0
+    for X in pins.random_hexes(200, 0.45, 3):
+        c = oracle.samples27(X)
+        ref = pins.detj(X, nodes)
+        assert np.max(np.abs(c - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+def test_bezier_expansion_reproduces_detj():
+    """sum_sigma b_sigma B_sigma(xi) = det J(xi) everywhere (Eq. e:bezExpansion)."""
+    rng = np.random.default_rng(4)
+    for X in pins.random_hexes(200, 0.45, 4):
+        b = oracle.check_hex(X)["b"]
+        P = rng.uniform(0, 1, size=(50, 3))
+        ref = pins.detj(X, P)
+        got = pins.bezier_eval(b, P)
+        assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(b))
+        # and the oracle's own evaluator agrees with the independent one
+        for p in P[:5]:
+            assert abs(oracle.bezier_eval(b, p) - pins.bezier_eval(b, p[None])[0]) <= 1e-14 * np.max(np.abs(b))
+
+
+def test_corner_coefficients_are_corner_tet_determinants():
+    """b_1..8 = det J at corners = 6 vol(corner tet)."""
+    for X in pins.random_hexes(100, 0.4, 5):
+        b = oracle.check_hex(X)["b"]
+        for k in range(8):
+            kap = pins.KAPPA[k]
+            nbrs = []
+            for a in range(3):
+                nb = kap.copy()
+                nb[a] = 1 - nb[a]
+                nbrs.append(int(np.nonzero((pins.KAPPA == nb).all(axis=1))[0][0]))
+            d = pins.tet_det(X[k], X[nbrs[0]], X[nbrs[1]], X[nbrs[2]])
+            flips = int(np.sum(kap))                  # each flipped axis reverses one edge
+            assert abs(b[k] - (-1) ** flips * d) <= 1e-13 * max(1.0, abs(d))
+
+
+def test_mean_coefficient_is_volume():
+    """mean(b) = integral of det J = hex volume (10 tets; quadrature)."""
+    for X in pins.random_hexes(100, 0.4, 6):
+        b = oracle.check_hex(X)["b"]
+        v10 = pins.volume_10_tets(X)
+        vq = pins.volume_quadrature(X)
+        assert abs(b.mean() - v10) <= 1e-13 * np.max(np.abs(b))
+        assert abs(b.mean() - vq) <= 1e-12 * np.max(np.abs(b))
+
+
+# --------------------------------------------------------------------------
+# closed forms
+# --------------------------------------------------------------------------
+
+def test_unit_cube_valid_no_subdivision():
+    r = oracle.check_hex(U)
+    assert r["flags"] == oracle.VALID and r["nodes"] == 0
+    assert np.all(r["b"] == 1.0)
+
+
+def test_mirrored_cube_invalid():
+    X = U.copy()
+    X[:, 0] *= -1.0
+    r = oracle.check_hex(X)
+    assert r["flags"] == oracle.INVALID
+    assert np.all(r["b"] == -1.0)
+
+
+def test_parallelepiped_all_coefficients_equal():
+    """Affine map => det J constant => all 27 b equal det A."""
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        A = rng.normal(size=(3, 3))
+        x0 = rng.normal(size=3)
+        X = U @ A.T + x0
+        r = oracle.check_hex(X)
+        d = np.linalg.det(A)
+        assert np.max(np.abs(r["b"] - d)) <= 1e-13 * max(1.0, np.max(np.abs(A)) ** 3)
+        assert (r["flags"] & 3) == (oracle.VALID if d > 0 else oracle.INVALID)
+        assert r["nodes"] == 0
+
+
+def test_power_of_two_scaling_is_exact():
+    """Scaling by 2^k scales every det J value by 8^k exactly; the verdict is unchanged."""
+    for X in pins.random_hexes(100, 0.45, 8):
+        r0 = oracle.check_hex(X)
+        r1 = oracle.check_hex(X * 4.0)
+        assert r1["flags"] == r0["flags"]
+        assert np.array_equal(r1["b"], r0["b"] * 64.0)
+
+
+# --------------------------------------------------------------------------
+# subdivision
+# --------------------------------------------------------------------------
+
+def test_subdivision_is_exact_reparameterisation():
+    rng = np.random.default_rng(9)
+    for _ in range(100):
+        b = rng.normal(size=27)
+        for o in range(8):
+            child = oracle.subdivide(b, o)
+            kap = pins.KAPPA[o]
+            loc = rng.uniform(0, 1, size=(20, 3))
+            glob = 0.5 * (kap[None, :] + loc)
+            assert np.max(np.abs(pins.bezier_eval(child, loc) - pins.bezier_eval(b, glob))) <= 1e-14 * np.max(np.abs(b))
+
+
+def test_subdivision_children_corners_are_values():
+    """Child corner coefficients are actual values of the polynomial."""
+    rng = np.random.default_rng(10)
+    b = rng.normal(size=27)
+    for o in range(8):
+        child = oracle.subdivide(b, o)
+        kap = pins.KAPPA[o]
+        for k in range(8):
+            pt = 0.5 * (kap + pins.KAPPA[k])
+            assert abs(child[k] - pins.bezier_eval(b, pt[None])[0]) <= 1e-14 * np.max(np.abs(b))
+
+
+def test_depth_cap_gives_undetermined():
+    """A polynomial >= 0 with a zero at a non-dyadic point never decides: depth cap -> UNDETERMINED."""
+    a = 1.0 / 3.0
+    q = np.array([a * a, a * (a - 1.0), (1.0 - a) ** 2])     # Bernstein coefficients of (t-a)^2
+    b = np.array([q[i] + q[j] + q[k] for i, j, k in pins.XI2])
+    r = oracle.classify_coeffs(b, 1.0)
+    assert r["flags"] == (oracle.UNDETERMINED | oracle.FLAG_SUBDIVIDED)
+    assert r["max_depth"] == oracle.MAX_DEPTH
+    # shifted upwards by a margin, the same polynomial is VALID after subdivision
+    r2 = oracle.classify_coeffs(b + 1e-3, 1.0)
+    assert r2["flags"] == (oracle.VALID | oracle.FLAG_SUBDIVIDED)
+
+
+def test_invalid_dominates_undetermined():
+    """A negative child corner anywhere gives INVALID even if another branch caps (reading G4)."""
+    a = 1.0 / 3.0
+    q = np.array([a * a, a * (a - 1.0), (1.0 - a) ** 2])
+    b = np.array([q[i] + q[j] + q[k] for i, j, k in pins.XI2])
+    b[26] = -5.0          # centre coefficient very negative: det < 0 near the centre
+    r = oracle.classify_coeffs(b, 1.0)
+    assert (r["flags"] & 3) == oracle.INVALID
+    assert pins.bezier_eval(b, r["witness"][None])[0] <= 0.0
+
+
+# --------------------------------------------------------------------------
+# the paper's examples (Figs. 5-7)
+# --------------------------------------------------------------------------
+
+def test_fig5_invalid_with_27_positive_samples(golden_hexes):
+    X, exp = golden_hexes["fig5_invalid"]
+    r = oracle.check_hex(X)
+    assert (r["flags"] & 3) == oracle.INVALID and exp["verdict"] == "INVALID"
+    assert np.all(pins.detj(X, pins.XI2 / 2.0) > 0)          # caption: positive at the 27 nodes
+    assert np.all(r["c"] > 0)
+    assert r["subdivided"] == 1                                # decided by recursive_subdivision
+    assert pins.detj(X, r["witness"][None])[0] <= 0.0          # witness really is non-positive
+
+
+def test_fig6_valid(golden_hexes):
+    X, exp = golden_hexes["fig6_valid"]
+    r = oracle.check_hex(X)
+    assert exp["verdict"] == "VALID"
+    assert (r["flags"] & 3) == oracle.VALID
+    assert r["subdivided"] == 1 and np.min(r["b"]) < 0        # needs subdivision to prove validity
+    P = pins.grid_points(40)
+    assert np.min(pins.detj(X, P)) > 0
+
+
+def test_fig7_invalid_at_step2_with_high_corner_quality(golden_hexes):
+    X, exp = golden_hexes["fig7_invalid"]
+    r = oracle.check_hex(X)
+    assert exp["verdict"] == "INVALID"
+    assert r["flags"] == oracle.INVALID                        # Step 2, not subdivided
+    assert np.all(r["c"][:8] > 0) and np.min(r["c"][8:20]) < 0
+    assert abs(pins.corner_scaled_jacobian(X) - float(exp["corner_scaled_jacobian"])) <= 0.01
+
+
+# --------------------------------------------------------------------------
+# brute force and exactness
+# --------------------------------------------------------------------------
+
+def test_brute_force_never_contradicts():
+    """Dense sampling of det J never contradicts a verdict (SURVEY.md 4 pin 8)."""
+    P = pins.grid_points(16)
+    adv, _ = hexgen.adversarial_config(200, seed=4, start=5000)
+    Xs = np.concatenate([pins.random_hexes(150, 0.5, 11), pins.random_hexes(150, 0.6, 12),
+                         hexgen.soa_to_nodes(adv)])
+    seen = set()
+    for X in Xs:
+        r = oracle.check_hex(X)
+        v = r["flags"] & 3
+        seen.add((v, r["subdivided"]))
+        E3 = r["E"] ** 3
+        if v == oracle.VALID:
+            assert np.min(pins.detj(X, P)) > -1e-12 * E3
+        elif v == oracle.INVALID:
+            assert pins.detj(X, r["witness"][None])[0] <= 1e-12 * E3
+    assert (oracle.VALID, 1) in seen and (oracle.INVALID, 1) in seen and (oracle.INVALID, 0) in seen
+
+
+def _degenerate_hexes(rng, n):
+    """Hexes with duplicated or coplanar vertices: det J values exactly 0 at some nodes."""
+    out = []
+    for _ in range(n):
+        X = U + rng.uniform(-0.3, 0.3, size=(8, 3))
+        kind = rng.integers(0, 3)
+        i, j = rng.choice(8, size=2, replace=False)
+        if kind == 0:
+            X[j] = X[i]                                  # duplicate vertex
+        elif kind == 1:
+            X[j] = X[i] + 0.5 * (X[(i + 1) % 8] - X[i])  # point on a segment (rounded)
+        else:
+            X[:, 2] = np.round(X[:, 2] * 8) / 8          # many coplanar dyadic points
+            X[j, 2] = X[i, 2]
+        out.append(X)
+    return out
+
+
+def test_exact_sign_matches_rational_arithmetic():
+    """The oracle's bigint sign of det J(xi_sigma) equals Python exact rationals."""
+    rng = np.random.default_rng(13)
+    hexes = _degenerate_hexes(rng, 60) + list(pins.random_hexes(20, 0.4, 14))
+    zeros = 0
+    for X in hexes:
+        for s in range(27):
+            ex = pins.detj_exact(X, s)
+            sg = (ex > 0) - (ex < 0)
+            zeros += sg == 0
+            assert oracle.exact_sign(X, s) == sg, (s, X)
+    assert zeros > 20
+
+
+def test_exact_zero_sample_is_invalid():
+    """A sample exactly 0 (diagonal duplicate) is decided INVALID although fp gives +-tiny (reading G2/G8)."""
+    rng = np.random.default_rng(15)
+    hits = 0
+    for _ in range(200):
+        X = U + rng.uniform(-0.3, 0.3, size=(8, 3))
+        X[2] = X[0]                       # nodes 1 and 3 coincide: det J = 0 at corner 2
+        r = oracle.check_hex(X)
+        assert pins.detj_exact(X, 1) == 0
+        assert (r["flags"] & 3) == oracle.INVALID
+        if r["c"][1] != 0.0:
+            hits += 1
+            assert r["exact_used"] >= 1
+    assert hits > 0
+
+
+def test_nonfinite_and_out_of_range():
+    for bad in (np.nan, np.inf, -np.inf, 2.0 ** 301):
+        X = U.copy()
+        X[5, 1] = bad
+        assert oracle.check_hex(X)["flags"] == oracle.NONFINITE
+    X = U * 2.0 ** 299
+    assert oracle.check_hex(X)["flags"] == oracle.VALID
+
+
+# --------------------------------------------------------------------------
+# closed-form families (config 4) and batch driver
+# --------------------------------------------------------------------------
+
+def test_adversarial_families_closed_form_verdicts():
+    """Pushed-corner and twisted-prism families: VALID iff r > 0 (DESIGN.md input recipe)."""
+    coords, r = hexgen.adversarial_config(600, seed=4, start=0)
+    o = oracle.check_soa(coords, nthreads=0)
+    v = o["flags"] & 3
+    assert np.array_equal(v, np.where(r > 0, oracle.VALID, oracle.INVALID))
+    even = np.arange(600) % 2 == 0
+    assert not np.any(o["flags"][even] & oracle.FLAG_SUBDIVIDED)    # multilinear: never subdivides
+    assert np.mean((o["flags"][~even] & oracle.FLAG_SUBDIVIDED) > 0) > 0.9
+    assert not np.any(o["near"])
+
+
+def test_twisted_valid_node_count_is_order_independent():
+    """For VALID hexes the subdivision tree is fully explored: node count equals that of a
+    breadth-first count done here."""
+    coords, r = hexgen.adversarial_config(40, seed=4, start=1001)
+    nodes = hexgen.soa_to_nodes(coords)
+    for X, rr in zip(nodes[0::2], r[0::2]):          # start is odd: even positions are twisted prisms
+        res = oracle.check_hex(X)
+        if (res["flags"] & 3) != oracle.VALID or not res["subdivided"]:
+            continue
+        count, frontier = 0, [(res["b"], 0)]
+        while frontier:
+            nxt = []
+            for b, d in frontier:
+                count += 1
+                for o in range(8):
+                    ch = oracle.subdivide(b, o)
+                    assert np.min(ch[:8]) > 0
+                    if np.min(ch[8:]) > 0:
+                        continue
+                    assert d + 1 < oracle.MAX_DEPTH
+                    nxt.append((ch, d + 1))
+            frontier = nxt
+        assert count == res["nodes"]
+        if count > 50:
+            return
+    pytest.fail("no large valid twisted hex in the sample")
+
+
+def test_batch_equals_single():
+    coords = hexgen.soa_config(500, 0.4, 99)
+    o = oracle.check_soa(coords, want_coeffs=True, nthreads=4)
+    X = hexgen.soa_to_nodes(coords)
+    for i in range(0, 500, 7):
+        r = oracle.check_hex(X[i])
+        assert o["flags"][i] == r["flags"]
+        assert np.array_equal(o["coeffs"][:, i], r["b"])
+
+
+def test_config0_has_no_near_boundary_hexes():
+    _, coords = hexgen.make(0)
+    o = oracle.check_soa(coords)
+    assert o["near"].sum() == 0
+    f = o["flags"]
+    assert np.all((f & 3) != oracle.UNDETERMINED)
