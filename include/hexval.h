@@ -1,0 +1,159 @@
+/*
+ * hexval.h -- C ABI of the B200 hot path for the robust validity check of
+ * linear hexahedra (Johnen, Weill, Remacle, "Robust and efficient validation
+ * of the linear hexahedral element", IMR26 2017 = /root/reference/PAPER.md).
+ *
+ * Problem statement: "takes the coordinates of 8
+ * points as input and outputs the validity of the hexahedron".  A hexahedron
+ * is VALID iff its Jacobian determinant det J is strictly positive on the
+ * whole reference cube [0,1]^3 (Eq. e:det3d 416-423).
+ *
+ * Per hex the library runs the algorithm of PAPER.md section 6
+ * (lines 1105-1145):
+ *   1. the 20 Jacobian samples (8 corners, 12 edge midpoints) as tetrahedron
+ *      determinants (section 5);
+ *   2. any sample <= 0 -> INVALID (samples within their rounding bound of 0
+ *      are decided in exact arithmetic, reading G8);
+ *   3. the 27 Bezier coefficients b = T~ c20 (Table 3);
+ *   4. all of b_9..b_27 > 0 -> VALID;
+ *   5. otherwise recursive_subdivision(b): de Casteljau octree subdivision,
+ *      depth cap HEXVAL_MAX_DEPTH (children at that depth are classified but
+ *      not split; an undecided one makes the hex UNDETERMINED).
+ *
+ * Everything runs on one CUDA device in hand-written sm_100a kernels; there
+ * is no CPU fallback.  All entry points are plain C: host/device pointers,
+ * sizes and a cudaStream_t (no framework types).
+ */
+#ifndef HEXVAL_H
+#define HEXVAL_H
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (return values; never thrown) ------------------------ */
+#define HEXVAL_OK               0
+#define HEXVAL_ERR_ARGUMENT    (-1)  /* n < 0, n > INT32_MAX, or NULL with n > 0 */
+#define HEXVAL_ERR_ALIGNMENT   (-2)  /* a double/int pointer not 8/4-byte aligned */
+#define HEXVAL_ERR_CUDA        (-3)  /* launch / configuration / copy error */
+#define HEXVAL_ERR_ALLOC       (-4)  /* scratch allocation failed */
+
+/* ---- per-hex flags byte ----------------------------------------------------
+ * bits 0-1: verdict, bit 2: SUBDIVIDED (root undecided after Step 4, i.e.
+ * recursive_subdivision was entered), bits 3-7: zero.                       */
+#define HEXVAL_INVALID          0
+#define HEXVAL_VALID            1
+#define HEXVAL_UNDETERMINED     2    /* depth cap reached, no INVALID found  */
+#define HEXVAL_NONFINITE        3    /* a coordinate is NaN/Inf or |x| > 2^300 */
+#define HEXVAL_FLAG_SUBDIVIDED  4
+#define HEXVAL_MAX_DEPTH        20
+
+/* Device-side counters, accumulated with atomics when a pointer is passed to
+ * the *_ex calls.  The caller allocates it in device memory and zeroes it. */
+typedef struct hexval_stats {
+    unsigned long long n_valid;          /* final verdict counts            */
+    unsigned long long n_invalid;
+    unsigned long long n_undetermined;
+    unsigned long long n_nonfinite;
+    unsigned long long n_subdivided;     /* hexes with SUBDIVIDED set       */
+    unsigned long long n_exact;          /* hexes whose Step 2 needed exact signs */
+    unsigned long long n_nodes;          /* recursive_subdivision calls     */
+    unsigned long long max_depth;        /* deepest child depth classified  */
+} hexval_stats;
+
+/* Per-phase kernel timing (CUDA events recorded on the call's stream). */
+typedef struct hexval_profile hexval_profile;
+#define HEXVAL_PHASE_PASS1   0   /* pass-1 kernel: 20 dets, 27 coeffs, classify, compact */
+#define HEXVAL_PHASE_EXACT   1   /* exact-sign kernel for ambiguous root samples         */
+#define HEXVAL_PHASE_SUBDIV  2   /* subdivision kernel                                   */
+#define HEXVAL_NUM_PHASES    3
+
+/* ---- device-resident calls (asynchronous) ----------------------------------
+ * coords       SoA, 24 planes of n doubles: coords[(3*k + a)*n + i] is axis a
+ *              (x,y,z) of node k = 0..7 of hex i, nodes in Fig. 3 order
+ *              (bottom face 1-2-3-4 counter-clockwise, then
+ *              top face 5-6-7-8).  Device memory, 8-byte aligned.
+ * vertices     AoS xyz, vertices[3*v + a]; device memory, 8-byte aligned.
+ * hex_idx      row-major int32 [n][8] vertex ids in Fig. 3 order; device
+ *              memory, 4-byte aligned.  Precondition: 0 <= id < number of
+ *              vertices (not checked; there is no nv argument).
+ * flags_out    n bytes, device memory (see flags above).
+ * coeffs_out_opt  NULL or 27*n doubles, device memory, coefficient-major:
+ *              coeffs[s*n + i] = b_{s+1} of hex i in Fig. 3 order (b_1..8
+ *              corners, 9..20 edges, 21..26 faces, 27 centre), the Bezier
+ *              coefficients of det J (det J, i.e. 6 x volume, not volumes).
+ *              Written for every hex (also INVALID ones); unspecified for
+ *              NONFINITE hexes.
+ * stream       CUDA stream; all work is enqueued on it, results are valid
+ *              after the stream synchronises.  No host synchronisation
+ *              happens inside the call.  Calls on different streams are
+ *              independent (scratch is stream-ordered cudaMallocAsync).
+ * Ownership    the caller owns every buffer; the library never frees them.
+ * n == 0       returns HEXVAL_OK without enqueueing work.
+ * Returns      HEXVAL_OK or a negative status (see above).  Data problems
+ *              (NaN/Inf, out of range) are per-hex flags, never a status.   */
+int hexval_check_soa(const double* coords, int64_t n, uint8_t* flags_out,
+                     double* coeffs_out_opt, cudaStream_t stream);
+
+int hexval_check_indexed(const double* vertices, const int32_t* hex_idx, int64_t n,
+                         uint8_t* flags_out, double* coeffs_out_opt, cudaStream_t stream);
+
+/* Same, plus optional device stats (accumulated) and optional profile. */
+int hexval_check_soa_ex(const double* coords, int64_t n, uint8_t* flags_out,
+                        double* coeffs_out_opt, hexval_stats* stats_dev_opt,
+                        hexval_profile* profile_opt, cudaStream_t stream);
+
+int hexval_check_indexed_ex(const double* vertices, const int32_t* hex_idx, int64_t n,
+                            uint8_t* flags_out, double* coeffs_out_opt,
+                            hexval_stats* stats_dev_opt, hexval_profile* profile_opt,
+                            cudaStream_t stream);
+
+/* Steps 4-5 alone on caller-supplied Bezier coefficient
+ * vectors: coeffs is device memory, coefficient-major coeffs[s*n + i] (Fig. 3
+ * order, as coeffs_out above).  Item i is VALID if all of b_9..27 > 0, else
+ * recursive_subdivision runs on it (flags as above, SUBDIVIDED set).  As in the
+ * paper, Step 4 presumes the corner coefficients b_1..8 were already checked
+ * (they are only tested again as children's corners).  An item with a NaN/Inf
+ * coefficient gets NONFINITE.  Used for quality queries on arbitrary
+ * triquadratics and to pin the subdivision kernel in the tests.            */
+int hexval_classify_bezier(const double* coeffs, int64_t n, uint8_t* flags_out,
+                           hexval_stats* stats_dev_opt, cudaStream_t stream);
+
+/* ---- host-resident calls (synchronous, end to end) --------------------------
+ * Same layouts, but every pointer is HOST memory (pinned memory gives
+ * overlapped copies; pageable memory works but serialises).  The library
+ * copies the inputs to the device in chunks of chunk_hexes hexes (<= 0 picks
+ * a default), runs the device path on each chunk while the next chunk's copy
+ * is in flight (two internal streams), copies flags (and coefficients) back
+ * and returns after everything has landed in host memory.  `stream` orders
+ * the work after prior work on that stream (may be 0).                      */
+int hexval_check_soa_host(const double* coords_host, int64_t n, uint8_t* flags_host,
+                          double* coeffs_host_opt, int64_t chunk_hexes, cudaStream_t stream);
+
+int hexval_check_indexed_host(const double* vertices_host, int64_t nv,
+                              const int32_t* hex_idx_host, int64_t n, uint8_t* flags_host,
+                              double* coeffs_host_opt, int64_t chunk_hexes,
+                              cudaStream_t stream);
+
+/* ---- profiling ---------------------------------------------------------------
+ * create/destroy a profile object; pass it to *_ex; after synchronising the
+ * stream, hexval_profile_read() adds up the elapsed time of every recorded
+ * phase since the last read into ms_out[HEXVAL_NUM_PHASES] and the launch
+ * counts into launches_out[HEXVAL_NUM_PHASES] (either may be NULL), then
+ * resets.  Returns HEXVAL_OK or HEXVAL_ERR_CUDA.                           */
+hexval_profile* hexval_profile_create(void);
+void hexval_profile_destroy(hexval_profile* p);
+int hexval_profile_read(hexval_profile* p, double* ms_out, long long* launches_out);
+
+/* ---- misc -------------------------------------------------------------- */
+const char* hexval_status_string(int status);
+int hexval_version(void);              /* 100 * major + minor                */
+int hexval_kernel_launches_per_call(void); /* kernels one device call enqueues */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEXVAL_H */

@@ -1,0 +1,294 @@
+"""B200-native hot path of the robust validity check of linear hexahedra.
+
+Johnen, Weill, Remacle, "Robust and efficient validation of the linear
+hexahedral element" (IMR26 2017; /root/reference/PAPER.md).  Every step of the
+path runs in the hand-written sm_100a kernels of ``libhexval.so`` behind the C
+ABI declared in ``include/hexval.h``; this module only marshals arguments
+(ctypes) and uses PyTorch for device memory and streams.  There is no CPU
+fallback: importing the package fails loudly when the library is missing.
+
+Entry points mirror the C names:
+
+* :func:`check_soa` / :func:`check_indexed`           device tensors, async
+* :func:`check_soa_host` / :func:`check_indexed_host` host arrays, end to end
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = [
+    "INVALID", "VALID", "UNDETERMINED", "NONFINITE", "FLAG_SUBDIVIDED", "MAX_DEPTH",
+    "HexvalError", "lib", "library_path", "check_soa", "check_indexed", "check_soa_host",
+    "check_indexed_host", "classify_bezier", "Stats", "Profile", "status_string", "version",
+    "kernel_launches_per_call",
+]
+
+INVALID, VALID, UNDETERMINED, NONFINITE = 0, 1, 2, 3
+FLAG_SUBDIVIDED = 4
+MAX_DEPTH = 20
+PHASES = ("pass1", "exact", "subdiv")
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libhexval.so")
+
+
+class HexvalError(RuntimeError):
+    pass
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(_LIB_PATH):
+        raise HexvalError(
+            f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(_LIB_PATH)
+    L.hexval_check_soa.argtypes = [_vp, _i64, _vp, _vp, _vp]
+    L.hexval_check_indexed.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp]
+    L.hexval_check_soa_ex.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp]
+    L.hexval_check_indexed_ex.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
+    L.hexval_classify_bezier.argtypes = [_vp, _i64, _vp, _vp, _vp]
+    L.hexval_check_soa_host.argtypes = [_vp, _i64, _vp, _vp, _i64, _vp]
+    L.hexval_check_indexed_host.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp]
+    for f in ("hexval_classify_bezier", "hexval_check_soa", "hexval_check_indexed", "hexval_check_soa_ex", "hexval_check_indexed_ex",
+              "hexval_check_soa_host", "hexval_check_indexed_host", "hexval_version",
+              "hexval_kernel_launches_per_call"):
+        getattr(L, f).restype = ctypes.c_int
+    L.hexval_status_string.argtypes = [ctypes.c_int]
+    L.hexval_status_string.restype = ctypes.c_char_p
+    L.hexval_profile_create.argtypes = []
+    L.hexval_profile_create.restype = _vp
+    L.hexval_profile_destroy.argtypes = [_vp]
+    L.hexval_profile_destroy.restype = None
+    L.hexval_profile_read.argtypes = [_vp, _vp, _vp]
+    L.hexval_profile_read.restype = ctypes.c_int
+    return L
+
+
+_lib: ctypes.CDLL | None = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = _load()
+    return _lib
+
+
+def status_string(code: int) -> str:
+    return lib().hexval_status_string(int(code)).decode()
+
+
+def version() -> int:
+    return lib().hexval_version()
+
+
+def kernel_launches_per_call() -> int:
+    return lib().hexval_kernel_launches_per_call()
+
+
+def _check(code: int, what: str) -> None:
+    if code != 0:
+        raise HexvalError(f"{what} failed: {code} ({status_string(code)})")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_handle(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _require(t, dtype, name: str, ndim: int | None = None):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (use check_*_host for host memory)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must have {ndim} dims")
+
+
+class Stats:
+    """Device-side counters (``hexval_stats``) accumulated by the *_ex calls."""
+
+    FIELDS = ("n_valid", "n_invalid", "n_undetermined", "n_nonfinite", "n_subdivided",
+              "n_exact", "n_nodes", "max_depth")
+
+    def __init__(self, device=None):
+        torch = _torch()
+        self.buf = torch.zeros(len(self.FIELDS), dtype=torch.int64,
+                               device=device if device is not None else "cuda")
+
+    def zero_(self):
+        self.buf.zero_()
+        return self
+
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    def read(self) -> dict:
+        vals = self.buf.cpu().tolist()
+        return dict(zip(self.FIELDS, vals))
+
+
+class Profile:
+    """Per-phase kernel times recorded with CUDA events on the call's stream."""
+
+    def __init__(self):
+        self.h = lib().hexval_profile_create()
+        if not self.h:
+            raise HexvalError("hexval_profile_create failed")
+
+    def read(self) -> dict:
+        ms = (ctypes.c_double * 3)()
+        cnt = (ctypes.c_longlong * 3)()
+        _check(lib().hexval_profile_read(self.h, ms, cnt), "hexval_profile_read")
+        return {p: {"ms": ms[k], "launches": cnt[k]} for k, p in enumerate(PHASES)}
+
+    def close(self):
+        if self.h:
+            lib().hexval_profile_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def check_soa(coords, flags=None, coeffs=None, stats: Stats | None = None,
+              profile: Profile | None = None, stream=None):
+    """hexval_check_soa(_ex): coords is a (24, n) float64 CUDA tensor (plane p = 3*node + axis).
+
+    Returns ``(flags, coeffs)``; ``coeffs`` is a (27, n) tensor when ``coeffs``
+    is True or a preallocated tensor, else None.  Asynchronous on ``stream``
+    (default: torch's current stream).
+    """
+    torch = _torch()
+    _require(coords, torch.float64, "coords", 2)
+    if coords.shape[0] != 24:
+        raise ValueError("coords must have shape (24, n)")
+    n = coords.shape[1]
+    if flags is None:
+        flags = torch.empty(n, dtype=torch.uint8, device=coords.device)
+    _require(flags, torch.uint8, "flags")
+    if coeffs is True:
+        coeffs = torch.empty((27, n), dtype=torch.float64, device=coords.device)
+    elif coeffs is False:
+        coeffs = None
+    if coeffs is not None:
+        _require(coeffs, torch.float64, "coeffs")
+    rc = lib().hexval_check_soa_ex(coords.data_ptr(), n, flags.data_ptr(),
+                                   coeffs.data_ptr() if coeffs is not None else None,
+                                   stats.ptr() if stats is not None else None,
+                                   profile.h if profile is not None else None,
+                                   _stream_handle(stream))
+    _check(rc, "hexval_check_soa")
+    return flags, coeffs
+
+
+def check_indexed(vertices, hex_idx, flags=None, coeffs=None, stats: Stats | None = None,
+                  profile: Profile | None = None, stream=None):
+    """hexval_check_indexed(_ex): vertices (nv, 3) float64, hex_idx (n, 8) int32, CUDA tensors."""
+    torch = _torch()
+    _require(vertices, torch.float64, "vertices", 2)
+    _require(hex_idx, torch.int32, "hex_idx", 2)
+    if vertices.shape[1] != 3 or hex_idx.shape[1] != 8:
+        raise ValueError("vertices must be (nv, 3) and hex_idx (n, 8)")
+    n = hex_idx.shape[0]
+    if flags is None:
+        flags = torch.empty(n, dtype=torch.uint8, device=hex_idx.device)
+    _require(flags, torch.uint8, "flags")
+    if coeffs is True:
+        coeffs = torch.empty((27, n), dtype=torch.float64, device=hex_idx.device)
+    elif coeffs is False:
+        coeffs = None
+    if coeffs is not None:
+        _require(coeffs, torch.float64, "coeffs")
+    rc = lib().hexval_check_indexed_ex(vertices.data_ptr(), hex_idx.data_ptr(), n, flags.data_ptr(),
+                                       coeffs.data_ptr() if coeffs is not None else None,
+                                       stats.ptr() if stats is not None else None,
+                                       profile.h if profile is not None else None,
+                                       _stream_handle(stream))
+    _check(rc, "hexval_check_indexed")
+    return flags, coeffs
+
+
+def classify_bezier(coeffs, flags=None, stats: Stats | None = None, stream=None):
+    """hexval_classify_bezier: Steps 4-5 on a (27, n) float64 CUDA tensor of Bezier coefficients."""
+    torch = _torch()
+    _require(coeffs, torch.float64, "coeffs", 2)
+    if coeffs.shape[0] != 27:
+        raise ValueError("coeffs must have shape (27, n)")
+    n = coeffs.shape[1]
+    if flags is None:
+        flags = torch.empty(n, dtype=torch.uint8, device=coeffs.device)
+    _require(flags, torch.uint8, "flags")
+    rc = lib().hexval_classify_bezier(coeffs.data_ptr(), n, flags.data_ptr(),
+                                      stats.ptr() if stats is not None else None, _stream_handle(stream))
+    _check(rc, "hexval_classify_bezier")
+    return flags
+
+
+def _host_array(a, dtype, name):
+    """numpy array or (pinned) CPU tensor -> (pointer, keepalive)."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != dtype or not a.flags["C_CONTIGUOUS"]:
+            raise TypeError(f"{name} must be a C-contiguous {dtype} array")
+        return a.ctypes.data, a
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda or not a.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous CPU tensor")
+        return a.data_ptr(), a
+    raise TypeError(f"{name}: unsupported type {type(a)}")
+
+
+def check_soa_host(coords, flags, coeffs=None, chunk_hexes: int = 0, stream=None):
+    """hexval_check_soa_host: host (24, n) float64 in, host flags (and coeffs) out; synchronous."""
+    cp, _k1 = _host_array(coords, np.float64, "coords")
+    fp, _k2 = _host_array(flags, np.uint8, "flags")
+    kp = None
+    if coeffs is not None:
+        kp, _k3 = _host_array(coeffs, np.float64, "coeffs")
+    n = coords.shape[1]
+    rc = lib().hexval_check_soa_host(cp, n, fp, kp, int(chunk_hexes),
+                                     _stream_handle(stream) if stream is not None else 0)
+    _check(rc, "hexval_check_soa_host")
+    return flags
+
+
+def check_indexed_host(vertices, hex_idx, flags, coeffs=None, chunk_hexes: int = 0, stream=None):
+    vp, _k1 = _host_array(vertices, np.float64, "vertices")
+    ip, _k2 = _host_array(hex_idx, np.int32, "hex_idx")
+    fp, _k3 = _host_array(flags, np.uint8, "flags")
+    kp = None
+    if coeffs is not None:
+        kp, _k4 = _host_array(coeffs, np.float64, "coeffs")
+    nv = vertices.shape[0]
+    n = hex_idx.shape[0]
+    rc = lib().hexval_check_indexed_host(vp, nv, ip, n, fp, kp, int(chunk_hexes),
+                                         _stream_handle(stream) if stream is not None else 0)
+    _check(rc, "hexval_check_indexed_host")
+    return flags

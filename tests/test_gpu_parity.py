@@ -1,0 +1,283 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle (-m gpu).
+
+Flags must match bit for bit on every hex the oracle does not mark
+near-boundary (and configs 0-3 must have no near-boundary hexes).  Bezier
+coefficients must match within 1e-12 * max|b| of the hex (BASELINE.json
+north_star).  Full-size configs run on the GPU in the same launch
+configuration bench.py times; the oracle checks a sample of the outputs
+(random hexes plus every hex that took the exact-sign or subdivision path)
+and, for config 4, the closed-form verdict of every hex.
+"""
+import numpy as np
+import pytest
+
+import hexgen
+import oracle
+from tests import pins
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1706_01613_b200 as hv  # noqa: E402
+
+COEFF_TOL = 1e-12
+
+
+def gpu_soa(coords: np.ndarray, coeffs=False, stats=None):
+    dev = torch.from_numpy(np.ascontiguousarray(coords)).cuda()
+    f, k = hv.check_soa(dev, coeffs=coeffs, stats=stats)
+    torch.cuda.synchronize()
+    return f.cpu().numpy(), (k.cpu().numpy() if k is not None else None)
+
+
+def gpu_indexed(verts: np.ndarray, idx: np.ndarray, coeffs=False, stats=None):
+    v = torch.from_numpy(np.ascontiguousarray(verts)).cuda()
+    i = torch.from_numpy(np.ascontiguousarray(idx)).cuda()
+    f, k = hv.check_indexed(v, i, coeffs=coeffs, stats=stats)
+    torch.cuda.synchronize()
+    return f.cpu().numpy(), (k.cpu().numpy() if k is not None else None)
+
+
+def assert_flags_match(gpu_flags, ref, allow_near=False):
+    near = ref["near"].astype(bool)
+    if not allow_near:
+        assert near.sum() == 0, f"{near.sum()} near-boundary hexes"
+    bad = np.nonzero((gpu_flags != ref["flags"]) & ~near)[0]
+    assert bad.size == 0, (f"{bad.size} flag mismatches, first {bad[:10]}: "
+                           f"gpu {gpu_flags[bad[:10]]} oracle {ref['flags'][bad[:10]]}")
+
+
+def assert_coeffs_match(gpu_coeffs, ref_coeffs, flags):
+    ok = (flags & 3) != hv.NONFINITE
+    scale = np.max(np.abs(ref_coeffs), axis=0)
+    err = np.max(np.abs(gpu_coeffs - ref_coeffs), axis=0)
+    bad = np.nonzero(ok & (err > COEFF_TOL * scale))[0]
+    assert bad.size == 0, f"{bad.size} coefficient mismatches; worst rel {np.max(err[ok] / scale[ok])}"
+
+
+# --------------------------------------------------------------------------
+# paper examples and closed forms through the C ABI
+# --------------------------------------------------------------------------
+
+def test_paper_figures(golden_hexes):
+    X = np.stack([golden_hexes[k][0] for k in ("fig5_invalid", "fig6_valid", "fig7_invalid")])
+    coords = hexgen.nodes_to_soa(X)
+    f, k = gpu_soa(coords, coeffs=True)
+    assert (f & 3).tolist() == [hv.INVALID, hv.VALID, hv.INVALID]
+    assert f.tolist() == [hv.INVALID | hv.FLAG_SUBDIVIDED, hv.VALID | hv.FLAG_SUBDIVIDED, hv.INVALID]
+    ref = oracle.check_soa(coords, want_coeffs=True)
+    assert_flags_match(f, ref)
+    assert_coeffs_match(k, ref["coeffs"], f)
+
+
+def test_closed_forms():
+    rng = np.random.default_rng(1)
+    U = pins.KAPPA.astype(float)
+    hexes = [U, U * [2, 3, 4], U * [-1, 1, 1]]
+    for _ in range(50):
+        A = rng.normal(size=(3, 3))
+        hexes.append(U @ A.T + rng.normal(size=3))
+    X = np.stack(hexes)
+    f, k = gpu_soa(hexgen.nodes_to_soa(X), coeffs=True)
+    assert f[0] == hv.VALID and np.all(k[:, 0] == 1.0)
+    assert f[1] == hv.VALID and np.all(k[:, 1] == 24.0)
+    assert f[2] == hv.INVALID and np.all(k[:, 2] == -1.0)
+    for j in range(3, X.shape[0]):
+        d = np.linalg.det(X[j, [1, 3, 4]] - X[j, 0])
+        assert np.max(np.abs(k[:, j] - d)) <= 1e-13 * max(1.0, np.abs(X[j]).max() ** 3)
+        assert f[j] == (hv.VALID if d > 0 else hv.INVALID)
+
+
+def test_nonfinite_and_empty():
+    U = pins.KAPPA.astype(float)
+    X = np.stack([U.copy() for _ in range(6)])
+    X[0, 3, 1] = np.nan
+    X[1, 0, 0] = np.inf
+    X[2, 7, 2] = -np.inf
+    X[3, 5, 0] = 2.0 ** 301
+    X[4] *= 2.0 ** 299
+    f, _ = gpu_soa(hexgen.nodes_to_soa(X))
+    assert f.tolist() == [3, 3, 3, 3, 1, 1]
+    empty = torch.empty((24, 0), dtype=torch.float64, device="cuda")
+    fl, _ = hv.check_soa(empty)
+    torch.cuda.synchronize()
+    assert fl.numel() == 0
+
+
+# --------------------------------------------------------------------------
+# small configs, ragged sizes, exact path, subdivision
+# --------------------------------------------------------------------------
+
+def test_config0_full_parity():
+    _, coords = hexgen.make(0)
+    stats = hv.Stats()
+    f, k = gpu_soa(coords, coeffs=True, stats=stats)
+    ref = oracle.check_soa(coords, want_coeffs=True)
+    assert_flags_match(f, ref)
+    assert_coeffs_match(k, ref["coeffs"], f)
+    st = stats.read()
+    assert st["n_valid"] + st["n_invalid"] + st["n_undetermined"] + st["n_nonfinite"] == coords.shape[1]
+    assert st["n_subdivided"] == int(np.sum((f & 4) > 0))
+
+
+@pytest.mark.parametrize("n", [1, 31, 255, 256, 257, 1000, 3 * 256 + 37, 20011])
+def test_ragged_sizes_high_noise(n):
+    coords = hexgen.ragged_soa(n, seed=100 + n, amp=0.45)
+    f, k = gpu_soa(coords, coeffs=True)
+    ref = oracle.check_soa(coords, want_coeffs=True)
+    assert_flags_match(f, ref, allow_near=True)
+    assert ref["near"].sum() <= max(1, n // 5000)
+    assert_coeffs_match(k, ref["coeffs"], f)
+
+
+def test_subdivision_heavy_random_hexes():
+    """Amplitude 0.5 gives many subdivided hexes of both final verdicts."""
+    coords = hexgen.ragged_soa(200_000, seed=7, amp=0.5)
+    stats = hv.Stats()
+    f, _ = gpu_soa(coords, stats=stats)
+    ref = oracle.check_soa(coords)
+    assert_flags_match(f, ref, allow_near=True)
+    sub = (f & 4) > 0
+    assert sub.sum() > 50
+    assert np.any((f[sub] & 3) == hv.INVALID) and np.any((f[sub] & 3) == hv.VALID)
+    # node counts are order independent for VALID hexes: totals must agree
+    valid_sub = sub & ((f & 3) == hv.VALID)
+    st = stats.read()
+    assert st["n_subdivided"] == sub.sum()
+    assert st["n_nodes"] >= ref["nodes"][valid_sub].sum()
+
+
+def _degenerate_soa(n, seed):
+    rng = np.random.default_rng(seed)
+    U = pins.KAPPA.astype(float)
+    X = U[None] + rng.uniform(-0.3, 0.3, size=(n, 8, 3))
+    for h in range(n):
+        kind = h % 4
+        i, j = rng.choice(8, size=2, replace=False)
+        if kind == 0:
+            X[h, j] = X[h, i]                       # duplicate (maybe diagonal)
+        elif kind == 1:
+            X[h, 2] = X[h, 0]                       # nodes 1, 3 coincide: c2 exactly 0, fp +-tiny
+        elif kind == 2:
+            X[h, :, 2] = np.round(X[h, :, 2] * 4) / 4   # coplanar dyadic layers
+            X[h, j, 2] = X[h, i, 2]
+    return hexgen.nodes_to_soa(X)
+
+
+def test_exact_sign_path_degenerate_hexes():
+    coords = _degenerate_soa(4000, 3)
+    stats = hv.Stats()
+    f, k = gpu_soa(coords, coeffs=True, stats=stats)
+    ref = oracle.check_soa(coords, want_coeffs=True)
+    assert_flags_match(f, ref, allow_near=True)
+    assert ref["near"].sum() <= 4
+    assert stats.read()["n_exact"] > 100          # the K5 kernel really ran
+    assert ref["exact"].sum() > 100
+
+
+def test_classify_bezier_depth_cap_and_random():
+    """Steps 4-5 on given coefficients vs the oracle's classify_coeffs (UNDETERMINED, node counts)."""
+    a = 1.0 / 3.0
+    q = np.array([a * a, a * (a - 1.0), (1.0 - a) ** 2])
+    point_zero = np.array([q[i] + q[j] + q[k] for i, j, k in pins.XI2])
+    rng = np.random.default_rng(5)
+    B = [point_zero, point_zero + 1e-3]
+    for _ in range(3000):
+        b = rng.uniform(0.05, 1.0, size=27)
+        b[8 + rng.integers(0, 19, size=rng.integers(1, 4))] -= rng.uniform(0.0, 1.5)
+        B.append(b)
+    B = np.array(B).T.copy()                      # (27, m) coefficient-major
+    stats = hv.Stats()
+    f = hv.classify_bezier(torch.from_numpy(B).cuda(), stats=stats)
+    torch.cuda.synchronize()
+    f = f.cpu().numpy()
+    assert f[0] == (hv.UNDETERMINED | hv.FLAG_SUBDIVIDED)
+    assert f[1] == (hv.VALID | hv.FLAG_SUBDIVIDED)
+    ref_flags, nodes_full = [], 0
+    for j in range(B.shape[1]):
+        r = oracle.classify_coeffs(B[:, j], 1.0)
+        ref_flags.append(r["flags"])
+        if (r["flags"] & 3) != oracle.INVALID and not r["near_boundary"]:
+            nodes_full += r["nodes"]
+    ref_flags = np.array(ref_flags)
+    assert np.array_equal(f, ref_flags)
+    assert np.sum((f & 3) == hv.INVALID) > 100 and np.sum(f == (hv.VALID | 4)) > 100
+    assert stats.read()["n_nodes"] >= nodes_full
+
+
+def test_indexed_equals_soa_and_host_path():
+    verts, idx = hexgen.indexed_config(3, start=0, count=300_000)
+    coords = hexgen.indexed_to_soa(verts, idx)
+    f1, k1 = gpu_soa(coords, coeffs=True)
+    f2, k2 = gpu_indexed(verts, idx, coeffs=True)
+    assert np.array_equal(f1, f2)
+    assert np.array_equal(k1, k2)                 # same arithmetic, same bits
+    f3 = np.zeros(coords.shape[1], np.uint8)
+    hv.check_soa_host(coords, f3, chunk_hexes=70_000)
+    assert np.array_equal(f1, f3)
+    f4 = np.zeros(idx.shape[0], np.uint8)
+    k4 = np.zeros((27, idx.shape[0]))
+    hv.check_indexed_host(verts, idx, f4, coeffs=k4, chunk_hexes=100_003)
+    assert np.array_equal(f1, f4) and np.array_equal(k1, k4)
+
+
+# --------------------------------------------------------------------------
+# full-size configurations (launch configuration of bench.py)
+# --------------------------------------------------------------------------
+
+def _sample(n, flags, k, seed):
+    rng = np.random.default_rng(seed)
+    special = np.nonzero((flags & 4) > 0)[0]
+    return np.unique(np.concatenate([rng.choice(n, size=min(n, k), replace=False), special[:20000]]))
+
+
+def test_config1_full_size_sampled():
+    _, coords = hexgen.make(1)
+    n = coords.shape[1]
+    stats = hv.Stats()
+    f, _ = gpu_soa(coords, stats=stats)
+    st = stats.read()
+    assert st["n_valid"] + st["n_invalid"] + st["n_undetermined"] + st["n_nonfinite"] == n
+    sel = _sample(n, f, 30000, 1)
+    ref = oracle.check_soa(np.ascontiguousarray(coords[:, sel]))
+    assert_flags_match(f[sel], ref)
+    frac_sub = np.mean((f & 4) > 0)
+    assert 1e-6 < frac_sub < 1e-3                 # ~3.2e-5
+
+
+def test_config2_full_size_sampled():
+    _, verts, idx = hexgen.make(2)
+    f, _ = gpu_indexed(verts, idx)
+    sel = _sample(idx.shape[0], f, 30000, 2)
+    ref = oracle.check_indexed(verts, idx[sel])
+    assert_flags_match(f[sel], ref)
+
+
+def test_config3_full_size_sampled():
+    _, verts, idx = hexgen.make(3)
+    stats = hv.Stats()
+    f, _ = gpu_indexed(verts, idx, stats=stats)
+    n = idx.shape[0]
+    dup = np.nonzero(np.array([len(set(r)) < 8 for r in idx[:400_000].tolist()]))[0]
+    sel = np.unique(np.concatenate([_sample(n, f, 30000, 3), dup[:20000]]))
+    ref = oracle.check_indexed(verts, idx[sel])
+    assert_flags_match(f[sel], ref)
+    assert stats.read()["n_exact"] > 0
+
+
+def test_config4_full_size_closed_form_and_sampled():
+    _, coords, r = hexgen.make(4)
+    stats = hv.Stats()
+    f, _ = gpu_soa(coords, stats=stats)
+    verdict = f & 3
+    expect = np.where(r > 0, hv.VALID, hv.INVALID)
+    assert np.array_equal(verdict, expect)        # closed form, every hex
+    even = np.arange(r.size) % 2 == 0
+    assert not np.any(f[even] & 4)
+    rng = np.random.default_rng(4)
+    sel = np.unique(rng.choice(r.size, size=3000, replace=False))
+    ref = oracle.check_soa(np.ascontiguousarray(coords[:, sel]))
+    assert_flags_match(f[sel], ref)
