@@ -35,26 +35,44 @@ import numpy as np  # noqa: E402
 
 METRIC = "hexahedra validated/sec (fp64, 1 B200); % of HBM roofline; subdivision rate"
 UNIT = "hex/s"
-BYTES_PER_HEX = 193                 # 24 fp64 coordinates in + 1 flags byte out
 FALLBACK_HBM_GBS = 6650.0
-CONFIGS = {
-    0: ("config0: 10k perturbed unit cubes, SoA fp64, noise U[-0.25,0.25]^3, seed 0", 10_000, 0.25, 0),
-    1: ("config1: 10M perturbed unit cubes, SoA fp64, noise U[-0.35,0.35]^3, seed 1", 10_000_000, 0.35, 1),
+# fp64 operations per subdivision node: 147 new de Casteljau values, one add and one
+# multiply each; peak = 148 SMs x 64 FP64 lanes x 1.965 GHz
+FP64_OPS_PER_NODE = 294
+FP64_PEAK_GOPS = 148 * 64 * 1.965
+CONFIG_DESC = {
+    0: "config0: 10k perturbed unit cubes, SoA fp64, noise U[-0.25,0.25]^3, seed 0",
+    1: "config1: 10M perturbed unit cubes, SoA fp64, noise U[-0.35,0.35]^3, seed 1",
+    2: "config2: 200^3 structured grid, 201^3 vertices jittered +-0.3, int32 connectivity, seed 2",
+    3: "config3: 40M candidate hexes on a 100^3 jittered grid (+-0.2), p_swap 0.1, int32 connectivity, seed 3",
+    4: "config4: 4M adversarial SoA hexes (pushed-corner parallelepipeds + twisted prisms), seed 4",
+}
+L2_NOTE = {
+    0: "inputs 1.9 MB fit in L2 (small parity case; not a bench line)",
+    1: "no flush: 1.92 GB of input per step >> 126 MB L2",
+    2: "no flush: 256 MB connectivity per step >> L2; 195 MB vertex array partially L2-reused by design",
+    3: "no flush: 1.28 GB connectivity per step >> L2; 24 MB vertex array L2-resident by design",
+    4: "no flush: 768 MB of input per step >> L2",
 }
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", type=int, default=1, choices=sorted(CONFIGS))
+    p.add_argument("--config", type=int, default=1, choices=sorted(CONFIG_DESC))
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
-    return p.parse_args()
+    p.add_argument("--variant", choices=["ldg", "wtma"], default=None,
+                   help="pass-1 kernel variant for SoA inputs (sets HEXVAL_PASS1; default: the library's)")
+    args = p.parse_args()
+    if args.variant:
+        os.environ["HEXVAL_PASS1"] = args.variant
+    return args
 
 
 def measured_peaks():
@@ -107,7 +125,7 @@ class ClockSampler:
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.nv is not None:
@@ -162,30 +180,45 @@ def barrier(world: int):
 # ---------------------------------------------------------------------------
 # CPU oracle (baseline / reference arm)
 # ---------------------------------------------------------------------------
-def oracle_rate(cfg: int, seconds: float, start: int = 0):
-    """Time the oracle, as it stands, on a bounded prefix sample of the workload."""
+def oracle_sample(cfg: int, m: int, start: int = 0):
     import hexgen
     import oracle
-    desc, n, amp, seed = CONFIGS[cfg]
+    if cfg in (0, 1):
+        coords = hexgen.soa_config(m, 0.25 if cfg == 0 else 0.35, cfg, start)
+        return lambda: oracle.check_soa(coords)
+    if cfg == 4:
+        coords, _ = hexgen.adversarial_config(m, 4, start)
+        return lambda: oracle.check_soa(coords)
+    _, verts, idx = hexgen.make(cfg, start, m)
+    return lambda: oracle.check_indexed(verts, idx)
+
+
+def oracle_rate(cfg: int, seconds: float, start: int = 0):
+    """Time the oracle, as it stands, on a bounded prefix sample of the workload (all host threads)."""
+    import hexgen
+    import oracle
+    n = hexgen.config_size(cfg)
     cores = oracle.num_threads(0)
-    probe = hexgen.soa_config(min(n, 20_000), amp, seed, start)
-    oracle.check_soa(probe)                                   # warm (thread pool, page-in)
+    probe_n = min(n, 20_000)
+    run = oracle_sample(cfg, probe_n, start)
+    run()                                                     # warm (thread pool, page-in)
     t0 = time.perf_counter()
-    oracle.check_soa(probe)
-    r0 = probe.shape[1] / (time.perf_counter() - t0)
-    m = int(min(n, max(20_000, r0 * seconds)))
-    sample = hexgen.soa_config(m, amp, seed, start)
+    run()
+    r0 = probe_n / (time.perf_counter() - t0)
+    m = int(min(n, max(probe_n, r0 * seconds)))
+    run = oracle_sample(cfg, m, start)
     t0 = time.perf_counter()
-    oracle.check_soa(sample)
+    run()
     dt = time.perf_counter() - t0
     return {"value": m / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"hexes {start}..{start + m - 1} of {desc} ({m} hexes, {dt:.2f} s wall on {cores} threads)"}
+            "sample": f"hexes {start}..{start + m - 1} of {CONFIG_DESC[cfg]} ({m} hexes, {dt:.2f} s wall on {cores} threads)"}
 
 
 def run_reference(args, world, rank):
+    import hexgen
     if rank != 0:
         return 0
-    desc, n, amp, seed = CONFIGS[args.config]
+    n = hexgen.config_size(args.config)
     per_step = []
     for _ in range(args.warmup):
         oracle_rate(args.config, min(args.cpu_seconds, 2.0))
@@ -198,8 +231,9 @@ def run_reference(args, world, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "n_hexes": n, "layout": "soa",
-                   "note": "each step times the CPU oracle on a bounded prefix sample; ms_per_step is extrapolated to the full batch"},
+        "config": {"workload": CONFIG_DESC[args.config], "n_hexes": n,
+                   "layout": "indexed" if args.config in (2, 3) else "soa",
+                   "note": "each step times the CPU oracle (oracle/, as it stands) on a bounded prefix sample; ms_per_step is extrapolated to the full batch"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
                          "sample": last["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -212,27 +246,54 @@ def run_reference(args, world, rank):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def make_inputs(cfg: int, rank: int):
+    """Host arrays of this rank's shard (weak scaling: every rank its own n hexes)."""
+    import hexgen
+    n = hexgen.config_size(cfg)
+    if cfg in (0, 1):
+        return "soa", n, (hexgen.soa_config(n, 0.25 if cfg == 0 else 0.35, cfg, start=rank * n),)
+    if cfg == 4:
+        coords, _ = hexgen.adversarial_config(n, 4, start=rank * n)
+        return "soa", n, (coords,)
+    _, verts, idx = hexgen.make(cfg)
+    return "indexed", n, (verts, idx)
+
+
+def algorithmic_bytes(layout: str, n: int, arrays) -> int:
+    """Compulsory HBM bytes of one pass-1 launch: inputs once + 1 flag byte/hex."""
+    if layout == "soa":
+        return 193 * n
+    verts, idx = arrays
+    return 32 * n + 24 * verts.shape[0] + n
+
+
 def run_ours(args, world, rank, local):
     import torch
 
-    import hexgen
     import paper_1706_01613_b200 as hv
 
     torch.cuda.set_device(local)
-    desc, n, amp, seed = CONFIGS[args.config]
-    coords_h = hexgen.soa_config(n, amp, seed, start=rank * n)         # rank r: its own n hexes
-    coords = torch.from_numpy(coords_h).cuda()
+    cfg = args.config
+    desc = CONFIG_DESC[cfg]
+    layout, n, host = make_inputs(cfg, rank)
+    dev = [torch.from_numpy(a).cuda() for a in host]
     flags = torch.empty(n, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
+    def step(profile=None, stats=None):
+        if layout == "soa":
+            hv.check_soa(dev[0], flags=flags, profile=profile, stats=stats)
+        else:
+            hv.check_indexed(dev[0], dev[1], flags=flags, profile=profile, stats=stats)
+
     # untimed: verdict / subdivision statistics of this workload
     stats = hv.Stats()
-    hv.check_soa(coords, flags=flags, stats=stats)
+    step(stats=stats)
     torch.cuda.synchronize()
     st = stats.read()
 
     for _ in range(args.warmup):
-        hv.check_soa(coords, flags=flags)
+        step()
     torch.cuda.synchronize()
 
     prof = hv.Profile()
@@ -243,73 +304,95 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            hv.check_soa(coords, flags=flags, profile=prof)
+            step(profile=prof)
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier(world)
     ms_total = ev0.elapsed_time(ev1)
     phases = prof.read()
     ms_step = dist_max(ms_total / args.steps, world)
-    pass1_ms = dist_max(phases["pass1"]["ms"] / max(1, phases["pass1"]["launches"]), world)
+    per = {k: v["ms"] / max(1, v["launches"]) for k, v in phases.items()}
+    pass1_ms = dist_max(per["pass1"], world)
+    subdiv_ms = dist_max(per["subdiv"], world)
 
     value = world * n / (ms_step * 1e-3)
     peak, peak_src = measured_peaks()
-    achieved = BYTES_PER_HEX * n / (pass1_ms * 1e-3) / 1e9
+    algo = algorithmic_bytes(layout, n, host)
+    achieved = algo / (pass1_ms * 1e-3) / 1e9
     traffic = ncu_traffic()
     roofline = {
-        "bound": "hbm", "kernel": "pass1_kernel<SoaLoader> (K1)",
+        "bound": "hbm", "kernel": "pass1 (K1 SoA warp-TMA staged / K2 indexed gather)",
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "peak_source": peak_src,
-        "algorithmic_bytes_per_launch": BYTES_PER_HEX * n,
-        "traffic": (traffic["dram_bytes_per_hex"] * n if traffic else None),
-        "traffic_source": (traffic.get("source") if traffic else None),
+        "algorithmic_bytes_per_launch": algo,
+        "traffic": (traffic["dram_bytes_per_hex"] * n if traffic and cfg == 1 else None),
+        "traffic_source": (traffic.get("source") if traffic and cfg == 1 else None),
         "frac_of_8TBs_nominal": achieved / 8000.0,
         "pass1_ms": pass1_ms,
         "pass1_share_of_step": pass1_ms / ms_step,
-        "phase_ms_per_step": {k: v["ms"] / max(1, v["launches"]) for k, v in phases.items()},
+        "phase_ms_per_step": per,
         "pass1_only_hex_per_s": n / (pass1_ms * 1e-3),
+        "timing": "CUDA events recorded by the library on the launching stream around each kernel, averaged over the timed steps",
+    }
+    subdivision = {
+        "rate": st["n_subdivided"] / n,
+        "nodes_per_step": st["n_nodes"],
+        "subdiv_kernel_ms": subdiv_ms,
+        "nodes_per_s": (st["n_nodes"] / (subdiv_ms * 1e-3)) if subdiv_ms > 0 and st["n_nodes"] else None,
+        "fp64_ops_per_node": FP64_OPS_PER_NODE,
+        "fp64_achieved_gops": (st["n_nodes"] * FP64_OPS_PER_NODE / (subdiv_ms * 1e-3) / 1e9) if subdiv_ms > 0 and st["n_nodes"] else None,
+        "fp64_peak_gops_at_max_clock": FP64_PEAK_GOPS,
     }
 
     # end to end through the host API: pinned inputs, H2D + kernels + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
-        del coords
+        del dev
         torch.cuda.empty_cache()
-        pin = torch.from_numpy(coords_h).pin_memory()
+        pins_ = [torch.from_numpy(a).pin_memory() for a in host]
         fl_h = torch.empty(n, dtype=torch.uint8).pin_memory()
-        hv.check_soa_host(pin, fl_h)                                   # warm
+
+        def host_step():
+            if layout == "soa":
+                hv.check_soa_host(pins_[0], fl_h)
+            else:
+                hv.check_indexed_host(pins_[0], pins_[1], fl_h)
+
+        host_step()                                                    # warm
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            hv.check_soa_host(pin, fl_h)
+            host_step()
         dt = time.perf_counter() - t0
         dt = dist_max(dt, world)
+        h2d = sum(a.nbytes for a in host)
         e2e = {"value": world * n * args.e2e_steps / dt, "unit": UNIT,
-               "h2d_bytes_per_step": 24 * 8 * n, "d2h_bytes_per_step": n,
-               "timing": "host wall clock around hexval_check_soa_host (synchronous; max over ranks)",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": n,
+               "timing": "host wall clock around the synchronous hexval_check_*_host call (H2D of pinned inputs, kernels, D2H of flags), max over ranks",
                "steps": args.e2e_steps}
-        fl_dev = flags.cpu()
-        if not torch.equal(fl_dev, fl_h):
+        if not torch.equal(flags.cpu(), fl_h):
             e2e["warning"] = "host-path flags differ from device-path flags"
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_rate(args.config, args.cpu_seconds)
+        cpu = oracle_rate(cfg, args.cpu_seconds)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "n_hexes_per_rank": n, "global_hexes": world * n, "layout": "soa",
+            "config": {"workload": desc, "n_hexes_per_rank": n, "global_hexes": world * n, "layout": layout,
                        "parallelism": f"independent shards x{world}" if world > 1 else "single GPU",
-                       "l2": "no flush: 1.92 GB of input per step per GPU >> 126 MB L2"},
+                       "l2": L2_NOTE[cfg],
+                       "pass1_variant": os.environ.get("HEXVAL_PASS1", "default")},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": hv.kernel_launches_per_call() * args.steps,
             "clocks": clk.summary(),
+            "subdivision": subdivision,
             "subdivision_rate": st["n_subdivided"] / n,
             "verdicts": {"valid": st["n_valid"], "invalid": st["n_invalid"],
                          "undetermined": st["n_undetermined"], "nonfinite": st["n_nonfinite"],

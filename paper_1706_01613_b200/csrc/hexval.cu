@@ -8,9 +8,10 @@
 //                        block-scan compaction of undecided / ambiguous hexes.
 //   K5    exact_kernel   exact signs of root samples within their rounding
 //                        bound of 0 (Kulisch accumulator), then Steps 3-4.
-//   K4    subdiv_kernel  persistent grid, dynamic hex fetch, per-thread
-//                        depth-first recursive_subdivision with a depth-20
-//                        frame stack in a global scratch buffer.
+//   K4    subdiv_kernel  persistent grid; each warp takes batches of 32 queued
+//                        hexes and splits up to 32 same-depth nodes per step
+//                        (one per lane), children pushed on a per-warp
+//                        depth-sorted stack in global memory.
 //
 // All launches go on the caller's stream; queue lengths are read on the
 // device, so there is no host synchronisation inside a call.
@@ -30,7 +31,7 @@ namespace {
 
 constexpr int P1_THREADS = 256;
 constexpr int K5_THREADS = 128;
-constexpr int K4_THREADS = 256;
+constexpr int K4_THREADS = 128;
 
 // flags placeholders written by pass 1 for hexes that later kernels finish
 constexpr uint8_t PENDING_EXACT = 0xFF;
@@ -57,6 +58,8 @@ struct SoaLoader {
 #pragma unroll
         for (int p = 0; p < 24; ++p) X[p] = __ldg(coords + (int64_t)p * n + i);
     }
+    // SoA has no connectivity: coincident nodes are found by the exact kernel
+    __device__ __forceinline__ bool dup_face_pair(int64_t) const { return false; }
 };
 
 struct IdxLoader {
@@ -81,6 +84,8 @@ struct IdxLoader {
         }
     }
     __device__ __forceinline__ void load_stream(int64_t i, double* X) const { load(i, X); }
+    // two nodes sharing a face have the same vertex id (see face_pair_coincident)
+    __device__ __forceinline__ bool dup_face_pair(int64_t i) const;
 };
 
 // NONFINITE (reading G13): a coordinate is NaN/Inf or |x| > 2^300
@@ -93,6 +98,37 @@ __device__ __forceinline__ bool out_of_range(const double* X) {
 #pragma unroll
     for (int p = 0; p < 24; ++p) bad |= !(fabs(X[p]) <= 0x1p300);
     return bad;
+}
+
+// Two nodes that share a face coincide (exact double equality of all three
+// coordinates) => some Step-2 sample is exactly 0 => INVALID (reading G2):
+//  * an edge pair makes a direct edge vector 0, and the corner samples at both
+//    ends contain it;
+//  * a face-diagonal pair (a, c) of face (a, b, c, d) makes the two in-face
+//    edge vectors at b (and at d) equal up to sign, so det J at corner b is 0.
+// Exact for every input; the exact kernel (K5) tests it before any long-accumulator work.
+__device__ __constant__ static const unsigned char kFacePairs[24][2] = {
+    {0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6}, {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7},   // edges
+    {0, 2}, {1, 3}, {4, 6}, {5, 7}, {0, 5}, {1, 4}, {1, 6}, {2, 5}, {2, 7}, {3, 6}, {0, 7}, {3, 4}};  // face diagonals
+
+__device__ __forceinline__ bool face_pair_coincident(const double* X) {
+    bool hit = false;
+#pragma unroll
+    for (int q = 0; q < 24; ++q) {
+        const int a = kFacePairs[q][0], b = kFacePairs[q][1];
+        hit |= (X[3 * a] == X[3 * b]) & (X[3 * a + 1] == X[3 * b + 1]) & (X[3 * a + 2] == X[3 * b + 2]);
+    }
+    return hit;
+}
+
+__device__ __forceinline__ bool IdxLoader::dup_face_pair(int64_t i) const {
+    int v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldg(idx + 8 * i + k);
+    bool hit = false;
+#pragma unroll
+    for (int q = 0; q < 24; ++q) hit |= v[kFacePairs[q][0]] == v[kFacePairs[q][1]];
+    return hit;
 }
 
 // Step 2 classification shared by pass 1 and the exact kernel.
@@ -122,75 +158,28 @@ __device__ __forceinline__ void write_coeffs(double* __restrict__ coeffs, int64_
     for (int sg = 0; sg < 27; ++sg) __stcs(coeffs + (int64_t)sg * n + i, P[kSigmaToSlot[sg]]);
 }
 
-// K3: warp ballot + block exclusive scan + one atomic per block
-template <int NW>
-__device__ __forceinline__ void block_append(bool pred, uint32_t val, uint32_t* __restrict__ q,
-                                             unsigned int* counter, unsigned int* s_warp) {
-    const int total = __syncthreads_count(pred);
-    if (total == 0) return;                            // block-uniform
+// K3, warp-aggregated: one atomic per warp that has something to append.
+__device__ __forceinline__ void warp_append(bool pred, uint32_t val, uint32_t* __restrict__ q, unsigned int* counter) {
     const unsigned bal = __ballot_sync(0xffffffffu, pred);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) s_warp[warp] = __popc(bal);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned run = 0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const unsigned c = s_warp[w];
-            s_warp[w] = run;
-            run += c;
-        }
-        s_warp[32] = atomicAdd(counter, run);
-    }
-    __syncthreads();
-    if (pred) q[s_warp[32] + s_warp[warp] + __popc(bal & ((1u << lane) - 1u))] = val;
+    if (bal == 0) return;                                   // warp-uniform
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(bal) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(bal));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) q[base + __popc(bal & ((1u << lane) - 1u))] = val;
 }
 
-// ---------------------------------------------------------------------------
-// K1 / K2: pass 1
-// ---------------------------------------------------------------------------
-template <class L, bool COEFFS, bool STATS>
-__global__ void __launch_bounds__(P1_THREADS) pass1_kernel(L ld, int64_t n, uint8_t* __restrict__ flags,
-                                                           double* __restrict__ coeffs, Ctl* ctl,
-                                                           uint32_t* __restrict__ qsub,
-                                                           uint32_t* __restrict__ qexact,
-                                                           hexval_stats* stats) {
-    __shared__ unsigned int s_sub[33], s_ex[33];
-    const int64_t i = (int64_t)blockIdx.x * P1_THREADS + threadIdx.x;
-    const bool active = i < n;
-    int st = -1;
-    if (active) {
-        double X[24];
-        ld.load_stream(i, X);
-        if (out_of_range(X)) {
-            st = ST_NONFINITE;
-        } else {
-            Samples s;
-            samples20(X, s);                                  // S1 + S2
-            st = step2_class(s, step2_tau(s.ekey));           // S3 (Step 2)
-            Coeffs t;
-            transform(s, t);                                  // S4 (Step 3)
-            if (st == ST_VALID && !step4_positive(t)) st = ST_SUB;   // S5 (Step 4)
-            if (COEFFS) write_coeffs(coeffs, n, i, s, t);
-        }
-        uint8_t f;
-        switch (st) {
-            case ST_INVALID: f = HEXVAL_INVALID; break;
-            case ST_VALID: f = HEXVAL_VALID; break;
-            case ST_NONFINITE: f = HEXVAL_NONFINITE; break;
-            case ST_SUB: f = HEXVAL_FLAG_SUBDIVIDED; break;
-            default: f = PENDING_EXACT; break;
-        }
-        __stcs(flags + i, f);
-    }
-    // S6: compaction into the two work queues
-    block_append<P1_THREADS / 32>(st == ST_SUB, (uint32_t)i, qsub, &ctl->n_sub, s_sub);
-    block_append<P1_THREADS / 32>(st == ST_EXACT, (uint32_t)i, qexact, &ctl->n_exact, s_ex);
+template <bool STATS>
+__device__ __forceinline__ void warp_epilogue(int st, int64_t i, Ctl* ctl, uint32_t* __restrict__ qsub,
+                                              uint32_t* __restrict__ qexact, hexval_stats* stats) {
+    warp_append(st == ST_SUB, (uint32_t)i, qsub, &ctl->n_sub);
+    warp_append(st == ST_EXACT, (uint32_t)i, qexact, &ctl->n_exact);
     if (STATS) {
-        const int nv = __syncthreads_count(st == ST_VALID);
-        const int ni = __syncthreads_count(st == ST_INVALID);
-        const int nn = __syncthreads_count(st == ST_NONFINITE);
-        if (threadIdx.x == 0) {
+        const unsigned nv = __popc(__ballot_sync(0xffffffffu, st == ST_VALID));
+        const unsigned ni = __popc(__ballot_sync(0xffffffffu, st == ST_INVALID));
+        const unsigned nn = __popc(__ballot_sync(0xffffffffu, st == ST_NONFINITE));
+        if ((threadIdx.x & 31) == 0) {
             if (nv) atomicAdd(&stats->n_valid, (unsigned long long)nv);
             if (ni) atomicAdd(&stats->n_invalid, (unsigned long long)ni);
             if (nn) atomicAdd(&stats->n_nonfinite, (unsigned long long)nn);
@@ -199,8 +188,201 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(L ld, int64_t n, uint
 }
 
 // ---------------------------------------------------------------------------
+// K1 / K2: pass 1
+// ---------------------------------------------------------------------------
+// S1-S5 + S8 for one hex whose 24 coordinates are in registers; returns the
+// pass-1 state (ST_*).
+template <bool COEFFS, class L>
+__device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i, int64_t n,
+                                         uint8_t* __restrict__ flags, double* __restrict__ coeffs) {
+    int st;
+    if (out_of_range(X)) {
+        st = ST_NONFINITE;
+    } else {
+        Samples s;
+        samples20(X, s);                                  // S1 + S2
+        st = step2_class(s, step2_tau(s.ekey));           // S3 (Step 2)
+        if (st == ST_EXACT && ld.dup_face_pair(i)) st = ST_INVALID;   // a sample is exactly 0
+        Coeffs t;
+        transform(s, t);                                  // S4 (Step 3)
+        if (st == ST_VALID && !step4_positive(t)) st = ST_SUB;   // S5 (Step 4)
+        if (COEFFS) write_coeffs(coeffs, n, i, s, t);
+    }
+    uint8_t f;
+    switch (st) {
+        case ST_INVALID: f = HEXVAL_INVALID; break;
+        case ST_VALID: f = HEXVAL_VALID; break;
+        case ST_NONFINITE: f = HEXVAL_NONFINITE; break;
+        case ST_SUB: f = HEXVAL_FLAG_SUBDIVIDED; break;
+        default: f = PENDING_EXACT; break;
+    }
+    __stcs(flags + i, f);
+    return st;
+}
+
+template <class L, bool COEFFS, bool STATS>
+__global__ void __launch_bounds__(P1_THREADS, 2) pass1_kernel(L ld, int64_t n, uint8_t* __restrict__ flags,
+                                                           double* __restrict__ coeffs, Ctl* ctl,
+                                                           uint32_t* __restrict__ qsub,
+                                                           uint32_t* __restrict__ qexact,
+                                                           hexval_stats* stats) {
+    const int64_t i = (int64_t)blockIdx.x * P1_THREADS + threadIdx.x;
+    int st = -1;
+    if (i < n) {
+        double X[24];
+        ld.load_stream(i, X);
+        st = pass1_hex<COEFFS>(ld, X, i, n, flags, coeffs);
+    }
+    warp_epilogue<STATS>(st, i, ctl, qsub, qexact, stats);
+}
+
+// ---------------------------------------------------------------------------
+// K1 (warp-TMA variant): persistent SoA pass 1.  Every warp owns two shared
+// memory buffers; lane 0 stages the 24 coordinate planes of the warp's next
+// 32-hex chunk with bulk async copies (cp.async.bulk + mbarrier complete_tx)
+// while the warp computes the current chunk, so each warp always has one
+// chunk (6 KB) in flight without spending registers on it, and no block-wide
+// barrier is needed (compaction is warp-aggregated).
+// ---------------------------------------------------------------------------
+constexpr int WT_THREADS = 256;
+constexpr int WT_WARPS = WT_THREADS / 32;
+constexpr int WT_ROW = 34;                        // doubles per staged plane row: 32 + room for an 8-B shift
+constexpr int WT_BUF = 24 * WT_ROW;               // doubles per buffer
+constexpr size_t WT_SMEM = (size_t)WT_WARPS * 2 * WT_BUF * sizeof(double);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
+// Stage chunk c (hexes 32c .. 32c+31, all < n) into buf.  Plane p starts at
+// element e = p*n + 32c; coords is 16-B aligned on this path, so e is odd
+// exactly when n and p are odd: then the copy starts one element early (an
+// element of plane p-1) and covers 34 doubles (272 B), and the reader shifts
+// by one.  With n odd a full chunk ends before n, so e + 32 <= 24n - 1.
+__device__ __forceinline__ void wt_issue(const double* __restrict__ coords, int64_t n, int64_t c, double* buf,
+                                         uint64_t* bar) {
+    const uint64_t policy = policy_evict_first();
+    const bool odd = n & 1;
+    mbar_expect_tx(bar, odd ? 12u * 256u + 12u * 272u : 24u * 256u);
+#pragma unroll 4
+    for (int p = 0; p < 24; ++p) {
+        const int64_t e = (int64_t)p * n + c * 32;
+        if (e & 1) bulk_g2s(buf + p * WT_ROW, coords + e - 1, 272u, bar, policy);
+        else bulk_g2s(buf + p * WT_ROW, coords + e, 256u, bar, policy);
+    }
+}
+
+template <bool COEFFS, bool STATS>
+__global__ void __launch_bounds__(WT_THREADS, 2)
+    pass1_soa_wtma_kernel(const double* __restrict__ coords, int64_t n, uint8_t* __restrict__ flags,
+                          double* __restrict__ coeffs, Ctl* ctl, uint32_t* __restrict__ qsub,
+                          uint32_t* __restrict__ qexact, hexval_stats* stats) {
+    extern __shared__ __align__(128) double wt_buf[];        // [warp][2][24][WT_ROW]
+    __shared__ __align__(8) uint64_t bars[WT_WARPS][2];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double* const mybuf = wt_buf + (size_t)wib * 2 * WT_BUF;
+    uint64_t* const mybar = bars[wib];
+    const int64_t n_full = n / 32;                           // full 32-hex chunks
+    const int64_t nw = (int64_t)gridDim.x * WT_WARPS;
+    const int64_t gw = (int64_t)blockIdx.x * WT_WARPS + wib;
+    const int shift = (int)(n & 1);
+    if (lane == 0) {
+        mbar_init(&mybar[0], 1);
+        mbar_init(&mybar[1], 1);
+        mbar_fence_init();
+        if (gw < n_full) wt_issue(coords, n, gw, mybuf, &mybar[0]);
+        if (gw + nw < n_full) wt_issue(coords, n, gw + nw, mybuf + WT_BUF, &mybar[1]);
+    }
+    __syncwarp();
+    int k = 0;
+    for (int64_t c = gw; c < n_full; c += nw, ++k) {
+        const int b = k & 1;
+        mbar_wait(&mybar[b], (unsigned)((k >> 1) & 1));
+        const double* src = mybuf + b * WT_BUF + lane;
+        double X[24];
+#pragma unroll
+        for (int p = 0; p < 24; ++p) X[p] = src[p * WT_ROW + (shift & p)];
+        const int64_t i = c * 32 + lane;
+        const int st = pass1_hex<COEFFS>(SoaLoader{coords, n}, X, i, n, flags, coeffs);
+        __syncwarp();                                        // every lane has consumed buffer b
+        if (lane == 0 && c + 2 * nw < n_full) wt_issue(coords, n, c + 2 * nw, mybuf + b * WT_BUF, &mybar[b]);
+        warp_epilogue<STATS>(st, i, ctl, qsub, qexact, stats);
+    }
+    // ragged tail (n mod 32 hexes): one warp, plain loads
+    if (n_full * 32 < n && gw == n_full % nw) {
+        const int64_t i = n_full * 32 + lane;
+        int st = -1;
+        if (i < n) {
+            double X[24];
+#pragma unroll
+            for (int p = 0; p < 24; ++p) X[p] = __ldcs(coords + (int64_t)p * n + i);
+            st = pass1_hex<COEFFS>(SoaLoader{coords, n}, X, i, n, flags, coeffs);
+        }
+        warp_epilogue<STATS>(st, i, ctl, qsub, qexact, stats);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K5: exact signs for ambiguous root samples, then Steps 3-4
 // ---------------------------------------------------------------------------
+// Steps 2-4 of one hex with exact signs for the samples within tau2 of 0
+// (PAPER.md:1114-1117); returns INVALID, VALID or FLAG_SUBDIVIDED (undecided
+// after Step 4).  Kept out of line: the long accumulator lives in local memory.
+__device__ __noinline__ uint8_t exact_resolve(const double* X) {
+    Samples s;
+    samples20(X, s);
+    const double tau2 = step2_tau(s.ekey);
+    double v[20];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = s.c[j];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) v[8 + e] = s.d[e];
+#pragma unroll 1
+    for (int j = 0; j < 20; ++j) {
+        if (v[j] < -tau2) return HEXVAL_INVALID;
+        if (fabs(v[j]) <= tau2 && exact_sample_sign(X, j) <= 0) return HEXVAL_INVALID;
+    }
+    Coeffs t;
+    transform(s, t);
+    return step4_positive(t) ? HEXVAL_VALID : HEXVAL_FLAG_SUBDIVIDED;
+}
+
 template <class L, bool STATS>
 __global__ void __launch_bounds__(K5_THREADS) exact_kernel(L ld, uint8_t* __restrict__ flags, Ctl* ctl,
                                                            const uint32_t* __restrict__ qexact,
@@ -210,33 +392,23 @@ __global__ void __launch_bounds__(K5_THREADS) exact_kernel(L ld, uint8_t* __rest
         const uint32_t h = qexact[q];
         double X[24];
         ld.load(h, X);
-        Samples s;
-        samples20(X, s);
-        const double tau2 = step2_tau(s.ekey);
-        bool invalid = false;
-        for (int j = 0; j < 20 && !invalid; ++j) {
-            const double x = j < 8 ? s.c[j] : s.d[j - 8];
-            if (x < -tau2) invalid = true;
-            else if (fabs(x) <= tau2) invalid = exact_sample_sign(X, j) <= 0;
-        }
         uint8_t f;
-        if (invalid) {
-            f = HEXVAL_INVALID;
+        if (face_pair_coincident(X)) {
+            f = HEXVAL_INVALID;                          // a Step-2 sample is exactly 0
         } else {
-            Coeffs t;
-            transform(s, t);
-            if (step4_positive(t)) {
-                f = HEXVAL_VALID;
-            } else {
-                f = HEXVAL_FLAG_SUBDIVIDED;
-                qsub[atomicAdd(&ctl->n_sub, 1u)] = h;
-            }
+            f = exact_resolve(X);
+            if (f == HEXVAL_FLAG_SUBDIVIDED) qsub[atomicAdd(&ctl->n_sub, 1u)] = h;
         }
         flags[h] = f;
-        if (STATS) {
-            atomicAdd(&stats->n_exact, 1ull);
-            if (f == HEXVAL_INVALID) atomicAdd(&stats->n_invalid, 1ull);
-            if (f == HEXVAL_VALID) atomicAdd(&stats->n_valid, 1ull);
+        if (STATS) {                                     // warp-aggregated counters
+            const unsigned am = __activemask();
+            const unsigned ninv = __popc(__ballot_sync(am, f == HEXVAL_INVALID));
+            const unsigned nval = __popc(__ballot_sync(am, f == HEXVAL_VALID));
+            if ((threadIdx.x & 31) == (unsigned)(__ffs(am) - 1)) {
+                atomicAdd(&stats->n_exact, (unsigned long long)__popc(am));
+                if (ninv) atomicAdd(&stats->n_invalid, (unsigned long long)ninv);
+                if (nval) atomicAdd(&stats->n_valid, (unsigned long long)nval);
+            }
         }
     }
 }
@@ -244,58 +416,38 @@ __global__ void __launch_bounds__(K5_THREADS) exact_kernel(L ld, uint8_t* __rest
 // ---------------------------------------------------------------------------
 // K4: recursive_subdivision, depth-first per thread
 // ---------------------------------------------------------------------------
-// Test the 8 children of node P; returns -1 if some child corner <= 0
-// (INVALID) else the bit mask (bit hx + 2 hy + 4 hz) of undecided children.
-__device__ __forceinline__ int test_children(const double* P) {
-    int pend = 0;
-    bool bad = false;
-    double G1[45];
-    both_split<0>(P, G1);
-#pragma unroll
-    for (int hx = 0; hx < 2; ++hx) {
-        double A[27];
-        take_half<0>(G1, hx, A);
-        double G2[45];
-        both_split<1>(A, G2);
-#pragma unroll
-        for (int hy = 0; hy < 2; ++hy) {
-            double B[27];
-            take_half<1>(G2, hy, B);
-            // zeta split of the 9 lines of B, classifying both children as the
-            // lines are produced (child hz takes points 2hz..2hz+2 of each line)
-            int mc0 = 0x7fffffff, mc1 = 0x7fffffff, mi0 = 0x7fffffff, mi1 = 0x7fffffff;
-#pragma unroll
-            for (int u = 0; u < 3; ++u)
-#pragma unroll
-                for (int w = 0; w < 3; ++w) {
-                    const double p0 = B[u + 3 * w], p1 = B[u + 3 * w + 9], p2 = B[u + 3 * w + 18];
-                    const double m01 = half_sum(p0, p1), m12 = half_sum(p1, p2), m = half_sum(m01, m12);
-                    const bool corner_line = (u != 1) && (w != 1);
-                    // child 0: (p0, m01, m); child 1: (m, m12, p2); points 0 and 2 of a
-                    // child line are corners iff the line itself is a corner line
-                    if (corner_line) {
-                        mc0 = min(mc0, min(key(p0), key(m)));
-                        mc1 = min(mc1, min(key(m), key(p2)));
-                    } else {
-                        mi0 = min(mi0, min(key(p0), key(m)));
-                        mi1 = min(mi1, min(key(m), key(p2)));
-                    }
-                    mi0 = min(mi0, key(m01));
-                    mi1 = min(mi1, key(m12));
-                }
-            bad |= (mc0 <= 0) | (mc1 <= 0);
-            const int b0 = hx + 2 * hy;
-            if (mi0 <= 0) pend |= 1 << b0;
-            if (mi1 <= 0) pend |= 1 << (b0 + 4);
-        }
-    }
-    return bad ? -1 : pend;
+// Warp-cooperative design: each warp owns a batch of up to 32 queued hexes
+// and a node stack in global memory (L2-resident in practice).  Every step the
+// 32 lanes split up to 32 nodes of the same depth (the top level of the
+// stack) into their 8 children (de Casteljau at t = 1/2 per axis, reading
+// G3), classify each child and push the undecided ones
+// with a warp prefix sum.  Only nodes of one depth are popped per step and
+// their children are pushed on top, so the stack is sorted by depth and holds
+// at most 32 x 8 = 256 nodes per level: K4_CAP = 19 x 256 nodes (levels
+// 1..19; children at depth 20 are classified but never pushed, reading G5).
+// Per-hex state (INVALID / depth cap reached) lives in shared memory; nodes of
+// a hex already found INVALID are dropped (the paper's early return).
+constexpr int K4_WARPS = K4_THREADS / 32;
+constexpr int K4_CAP = (MAX_DEPTH - 1) * 256;
+
+struct WarpStacks {
+    double* coef;           // [warp][27][K4_CAP], node layout i + 3j + 9k
+    unsigned char* owner;   // [warp][K4_CAP], batch slot (lane) of the node's hex
+};
+
+// One line (p0, p1, p2) split at t = 1/2: m01 = (p0+p1)/2, m = (p0+2p1+p2)/4,
+// m12 = (p1+p2)/2 (A.4 of SURVEY.md; 1 DMUL + 4 DFMA).
+__device__ __forceinline__ void line_split(double p0, double p1, double p2, double& m01, double& m, double& m12) {
+    const double h1 = __dmul_rn(0.5, p1);
+    m01 = __fma_rn(0.5, p0, h1);
+    m12 = __fma_rn(0.5, p2, h1);
+    m = __fma_rn(0.25, p0, __fma_rn(0.25, p2, h1));
 }
 
-struct Frames {
-    double* coef;        // [lvl][27][T]
-    unsigned char* mask; // [lvl][T]
-    unsigned T;
+struct K4Warp {
+    unsigned status[32];    // per batch slot: bit 0 INVALID found, bit 1 depth cap reached
+    uint32_t hex[32];       // hex id of each batch slot
+    int cnt[MAX_DEPTH + 1]; // nodes per level on the stack
 };
 
 // Root coefficients of queued item h: recomputed from the coordinates with
@@ -325,63 +477,179 @@ struct CoeffRoot {
 };
 
 template <class R, bool STATS>
-__global__ void __launch_bounds__(K4_THREADS, 1) subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
-                                                               const uint32_t* __restrict__ qsub, Frames fr,
-                                                               hexval_stats* stats) {
-    const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const unsigned T = fr.T;
+__global__ void __launch_bounds__(K4_THREADS) subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
+                                                            const uint32_t* __restrict__ qsub, WarpStacks ws,
+                                                            hexval_stats* stats) {
+    __shared__ K4Warp wst[K4_WARPS];
+    const int lane = threadIdx.x & 31;
+    K4Warp& W = wst[threadIdx.x >> 5];
+    const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
+    double* const sc = ws.coef + gw * 27 * K4_CAP;
+    unsigned char* const so = ws.owner + gw * K4_CAP;
     const unsigned total = *((volatile unsigned*)&ctl->n_sub);
-    double* const fc = fr.coef + tid;
-    unsigned char* const fm = fr.mask + tid;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    if (lane <= MAX_DEPTH) W.cnt[lane] = 0;
+    __syncwarp();
+    int top = 0, D = 0, nb = 0;                         // warp-uniform: stack size, top level, batch size
+    unsigned long long nodes = 0, n_inv = 0, n_val = 0, n_und = 0;
+    int maxd = 0;
     for (;;) {
-        const unsigned q = atomicAdd(&ctl->k4_next, 1u);
-        if (q >= total) break;
-        const uint32_t h = qsub[q];
         double P[27];
-        root(h, P);                                      // bit-identical to pass 1
-        unsigned long long nodes = 0;
-        int maxd = 0;
-        bool undet = false, invalid = false;
-        unsigned levels = 0;                             // bit d: frame d has pending children
-        int d = 0;                                       // depth of node P
-        for (;;) {
-            ++nodes;
-            // keep the node: its other undecided children are extracted from it later
-#pragma unroll
-            for (int c = 0; c < 27; ++c) fc[(size_t)(d * 27 + c) * T] = P[c];
-            int pend = test_children(P);
-            maxd = max(maxd, d + 1);
-            if (pend < 0) { invalid = true; break; }
-            if (pend && d + 1 >= MAX_DEPTH) { undet = true; pend = 0; }   // depth cap (reading G5)
-            int o;
-            if (pend) {
-                o = __ffs(pend) - 1;
-                pend &= pend - 1;
-                if (pend) { fm[(size_t)d * T] = (unsigned char)pend; levels |= 1u << d; }
-            } else {
-                // backtrack to the deepest frame with pending children
-                if (levels == 0) break;
-                d = 31 - __clz(levels);
-                unsigned m = fm[(size_t)d * T];
-                o = __ffs(m) - 1;
-                m &= m - 1;
-                if (m) fm[(size_t)d * T] = (unsigned char)m;
-                else levels &= ~(1u << d);
+        bool act;
+        int owner = lane, d;
+        if (top == 0) {
+            // batch done: write its verdicts (precedence INVALID > UNDETERMINED > VALID, reading G4)
+            if (lane < nb) {
+                const unsigned st = W.status[lane];
+                const uint8_t v = (st & 1u) ? HEXVAL_INVALID : ((st & 2u) ? HEXVAL_UNDETERMINED : HEXVAL_VALID);
+                flags[W.hex[lane]] = v | HEXVAL_FLAG_SUBDIVIDED;
+                if (STATS) { n_inv += v == HEXVAL_INVALID; n_val += v == HEXVAL_VALID; n_und += v == HEXVAL_UNDETERMINED; }
             }
-            double Pp[27];
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(&ctl->k4_next, 32u);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            nb = base < total ? (int)min(32u, total - base) : 0;
+            if (nb == 0) break;
+            act = lane < nb;
+            d = 0;
+            if (act) {
+                const uint32_t h = qsub[base + lane];
+                W.hex[lane] = h;
+                W.status[lane] = 0;
+                root(h, P);                              // bit-identical to pass 1
+            }
+        } else {
+            const int k = min(32, W.cnt[D]);
+            act = lane < k;
+            d = D;
+            if (act) {
+                const int slot = top - k + lane;
 #pragma unroll
-            for (int c = 0; c < 27; ++c) Pp[c] = fc[(size_t)(d * 27 + c) * T];
-            extract_child(Pp, o & 1, (o >> 1) & 1, o >> 2, P);
-            ++d;
+                for (int c = 0; c < 27; ++c) P[c] = sc[(size_t)c * K4_CAP + slot];
+                owner = so[slot];
+                act = (W.status[owner] & 1u) == 0;       // hex already INVALID: drop the node
+            }
+            top -= k;
+            __syncwarp();
+            if (lane == 0) W.cnt[D] -= k;
         }
-        const uint8_t verdict = invalid ? HEXVAL_INVALID : (undet ? HEXVAL_UNDETERMINED : HEXVAL_VALID);
-        flags[h] = verdict | HEXVAL_FLAG_SUBDIVIDED;
-        if (STATS) {
-            atomicAdd(&stats->n_subdivided, 1ull);
-            atomicAdd(&stats->n_nodes, nodes);
-            atomicMax(&stats->max_depth, (unsigned long long)maxd);
-            atomicAdd(verdict == HEXVAL_INVALID ? &stats->n_invalid
-                      : (verdict == HEXVAL_VALID ? &stats->n_valid : &stats->n_undetermined), 1ull);
+        __syncwarp();
+        const unsigned actmask = __ballot_sync(0xffffffffu, act);
+        if (STATS && actmask) { nodes += __popc(actmask); maxd = max(maxd, d + 1); }
+        // ---- split every active node into its 8 children --------------------
+        // xi split of P: G1[a + 5j + 15k], a = 0..4
+        double G1[45];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double p0 = P[3 * j + 9 * k], p1 = P[1 + 3 * j + 9 * k], p2 = P[2 + 3 * j + 9 * k];
+                double m01, m, m12;
+                line_split(p0, p1, p2, m01, m, m12);
+                double* g = G1 + 5 * j + 15 * k;
+                g[0] = p0; g[1] = m01; g[2] = m; g[3] = m12; g[4] = p2;
+            }
+        bool inval = false, capped = false;
+        int pushed = 0;                                  // warp-uniform
+        const bool can_push = d + 1 < MAX_DEPTH;
+#pragma unroll
+        for (int hx = 0; hx < 2; ++hx)
+#pragma unroll
+            for (int hy = 0; hy < 2; ++hy) {
+                // Z[a + 3u + 9v]: xi index a (0..2), eta index u (0..2), zeta index v (0..4)
+                double Z[45];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    double B[9];                         // B[u + 3k]: eta half hy of column a
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const double* g = G1 + 2 * hx + a + 15 * k;
+                        double m01, m, m12;
+                        line_split(g[0], g[5], g[10], m01, m, m12);
+                        if (hy == 0) { B[3 * k] = g[0]; B[1 + 3 * k] = m01; B[2 + 3 * k] = m; }
+                        else { B[3 * k] = m; B[1 + 3 * k] = m12; B[2 + 3 * k] = g[10]; }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 3; ++u) {
+                        double m01, m, m12;
+                        line_split(B[u], B[u + 3], B[u + 6], m01, m, m12);
+                        double* z = Z + a + 3 * u;
+                        z[0] = B[u]; z[9] = m01; z[18] = m; z[27] = m12; z[36] = B[u + 6];
+                    }
+                }
+                // classify the two children (zeta halves hz = 0, 1)
+                bool push[2];
+#pragma unroll
+                for (int hz = 0; hz < 2; ++hz) {
+                    int mc = 0x7fffffff, mi = 0x7fffffff;
+#pragma unroll
+                    for (int v = 0; v < 3; ++v)
+#pragma unroll
+                        for (int u = 0; u < 3; ++u)
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {
+                                const int kk = key(Z[a + 3 * u + 9 * (2 * hz + v)]);
+                                if (a != 1 && u != 1 && v != 1) mc = min(mc, kk);
+                                else mi = min(mi, kk);
+                            }
+                    const bool bad = act && mc <= 0;               // a corner value <= 0: INVALID
+                    const bool und = act && mc > 0 && mi <= 0;     // undecided child
+                    inval |= bad;
+                    capped |= und && !can_push;
+                    push[hz] = und && can_push;
+                }
+                const unsigned b0 = __ballot_sync(0xffffffffu, push[0] && !inval);
+                const unsigned b1 = __ballot_sync(0xffffffffu, push[1] && !inval);
+                if (b0 | b1) {
+                    const int c0 = __popc(b0);
+#pragma unroll
+                    for (int hz = 0; hz < 2; ++hz) {
+                        const unsigned bm = hz ? b1 : b0;
+                        if (bm & (1u << lane)) {
+                            const int slot = top + pushed + (hz ? c0 : 0) + __popc(bm & lt_mask);
+#pragma unroll
+                            for (int v = 0; v < 3; ++v)
+#pragma unroll
+                                for (int u = 0; u < 3; ++u)
+#pragma unroll
+                                    for (int a = 0; a < 3; ++a)
+                                        sc[(size_t)(a + 3 * u + 9 * v) * K4_CAP + slot] = Z[a + 3 * u + 9 * (2 * hz + v)];
+                            so[slot] = (unsigned char)owner;
+                        }
+                    }
+                    pushed += c0 + __popc(b1);
+                }
+            }
+        if (inval) atomicOr(&W.status[owner], 1u);
+        if (capped) atomicOr(&W.status[owner], 2u);
+        top += pushed;
+        __syncwarp();
+        if (pushed) {
+            if (lane == 0) W.cnt[d + 1] += pushed;
+            D = d + 1;
+        } else {
+            while (D > 0 && W.cnt[D] == 0) --D;           // W.cnt[D] was updated by lane 0 before the sync
+        }
+        __syncwarp();
+    }
+    if (STATS) {
+        // warp-aggregated counters
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            n_inv += __shfl_xor_sync(0xffffffffu, n_inv, o);
+            n_val += __shfl_xor_sync(0xffffffffu, n_val, o);
+            n_und += __shfl_xor_sync(0xffffffffu, n_und, o);
+        }
+        if (lane == 0) {
+            const unsigned long long nsub = n_inv + n_val + n_und;
+            if (nsub) {
+                atomicAdd(&stats->n_subdivided, nsub);
+                atomicAdd(&stats->n_nodes, nodes);
+                atomicMax(&stats->max_depth, (unsigned long long)maxd);
+                if (n_inv) atomicAdd(&stats->n_invalid, n_inv);
+                if (n_val) atomicAdd(&stats->n_valid, n_val);
+                if (n_und) atomicAdd(&stats->n_undetermined, n_und);
+            }
         }
     }
 }
@@ -392,11 +660,40 @@ __global__ void __launch_bounds__(K4_THREADS, 1) subdiv_kernel(R root, uint8_t* 
 struct DeviceInfo {
     int sms = 0;
     int k4_blocks_per_sm = 0;
+    bool p1_wtma = false;         // SoA pass 1: warp-TMA kernel (else the plain kernel)
+    int p1_ctas_per_sm = 1;
     bool ok = false;
 };
 
 DeviceInfo g_info[64];
 std::mutex g_info_mu;
+
+int wtma_setup() {
+    const void* fns[4] = {(const void*)pass1_soa_wtma_kernel<false, false>,
+                          (const void*)pass1_soa_wtma_kernel<false, true>,
+                          (const void*)pass1_soa_wtma_kernel<true, false>,
+                          (const void*)pass1_soa_wtma_kernel<true, true>};
+    for (const void* f : fns)
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WT_SMEM) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass1_soa_wtma_kernel<false, false>, WT_THREADS,
+                                                      WT_SMEM) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return occ;
+}
+
+// Pass-1 variant for SoA inputs: HEXVAL_PASS1 = ldg | wtma (tuning knob for
+// measurements; default wtma when the device supports its shared memory).
+int pass1_variant_from_env() {
+    const char* v = getenv("HEXVAL_PASS1");
+    if (v && !strcmp(v, "ldg")) return 0;
+    return 1;
+}
 
 template <class L>
 const DeviceInfo& device_info(int dev) {
@@ -407,6 +704,10 @@ const DeviceInfo& device_info(int dev) {
         int occ = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false>, K4_THREADS, 0);
         d.k4_blocks_per_sm = occ > 0 ? occ : 1;
+        const int want = pass1_variant_from_env();
+        const int ctas = want ? wtma_setup() : 0;
+        d.p1_wtma = ctas > 0;
+        d.p1_ctas_per_sm = ctas > 0 ? ctas : 1;
         // keep freed stream-ordered scratch in the pool between calls
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -430,6 +731,52 @@ struct hexval_profile {
 
 namespace {
 
+template <class L>
+void launch_pass1_plain(const L& ld, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl, uint32_t* qsub,
+                        uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
+    const unsigned blocks = (unsigned)((n + P1_THREADS - 1) / P1_THREADS);
+    if (coeffs) {
+        if (stats) pass1_kernel<L, true, true><<<blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_kernel<L, true, false><<<blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
+    } else {
+        if (stats) pass1_kernel<L, false, true><<<blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_kernel<L, false, false><<<blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
+    }
+}
+
+template <class L>
+void launch_pass1(const L& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl,
+                  uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
+    launch_pass1_plain(ld, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+}
+
+void launch_wtma(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl,
+                 uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
+    const int64_t chunks = (n + 31) / 32;
+    const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
+    const int64_t want = (chunks + WT_WARPS - 1) / WT_WARPS;
+    const unsigned grid = (unsigned)(want < cap ? want : cap);
+    const double* c = ld.coords;
+    if (coeffs) {
+        if (stats) pass1_soa_wtma_kernel<true, true><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_soa_wtma_kernel<true, false><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+    } else {
+        if (stats) pass1_soa_wtma_kernel<false, true><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_soa_wtma_kernel<false, false><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+    }
+}
+
+// SoA: the warp-TMA kernel when the coordinate array is 16-B aligned (bulk
+// copies need it), else the plain kernel.
+template <>
+void launch_pass1<SoaLoader>(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags,
+                             double* coeffs, Ctl* ctl, uint32_t* qsub, uint32_t* qex, hexval_stats* stats,
+                             cudaStream_t stream) {
+    const bool aligned = (((uintptr_t)ld.coords) & 15) == 0;
+    if (aligned && info.p1_wtma) launch_wtma(ld, info, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+    else launch_pass1_plain(ld, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+}
+
 int collect_profile(hexval_profile* p) {
     for (int k = 0; k < p->count; ++k)
         for (int ph = 0; ph < HEXVAL_NUM_PHASES; ++ph) {
@@ -449,14 +796,14 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return HEXVAL_ERR_CUDA;
     const DeviceInfo& info = device_info<L>(dev);
-    const unsigned T = (unsigned)(info.sms * info.k4_blocks_per_sm * K4_THREADS);
+    const size_t warps = (size_t)info.sms * info.k4_blocks_per_sm * K4_WARPS;
 
     if (prof && prof->count >= hexval_profile::CAP) return HEXVAL_ERR_ARGUMENT;   // read it first
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
-    const size_t fc_bytes = (size_t)MAX_DEPTH * 27 * T * sizeof(double);
-    const size_t fm_bytes = ((size_t)MAX_DEPTH * T + 255) & ~(size_t)255;
-    const size_t total = ctl_bytes + 2 * q_bytes + fc_bytes + fm_bytes;
+    const size_t sc_bytes = warps * 27 * K4_CAP * sizeof(double);
+    const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
+    const size_t total = ctl_bytes + 2 * q_bytes + sc_bytes + so_bytes;
     char* base = nullptr;
     if (cudaMallocAsync((void**)&base, total, stream) != cudaSuccess) {
         cudaGetLastError();
@@ -465,10 +812,9 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     Ctl* ctl = reinterpret_cast<Ctl*>(base);
     uint32_t* qsub = reinterpret_cast<uint32_t*>(base + ctl_bytes);
     uint32_t* qex = reinterpret_cast<uint32_t*>(base + ctl_bytes + q_bytes);
-    Frames fr;
+    WarpStacks fr;
     fr.coef = reinterpret_cast<double*>(base + ctl_bytes + 2 * q_bytes);
-    fr.mask = reinterpret_cast<unsigned char*>(base + ctl_bytes + 2 * q_bytes + fc_bytes);
-    fr.T = T;
+    fr.owner = reinterpret_cast<unsigned char*>(base + ctl_bytes + 2 * q_bytes + sc_bytes);
     cudaMemsetAsync(ctl, 0, ctl_bytes, stream);
 
     const int slot = prof ? prof->count++ : -1;
@@ -476,18 +822,11 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
         if (slot >= 0) cudaEventRecord(prof->ev[slot][ph][which], stream);
     };
 
-    const unsigned p1_blocks = (unsigned)((n + P1_THREADS - 1) / P1_THREADS);
     mark(HEXVAL_PHASE_PASS1, 0);
-    if (coeffs) {
-        if (stats) pass1_kernel<L, true, true><<<p1_blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_kernel<L, true, false><<<p1_blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
-    } else {
-        if (stats) pass1_kernel<L, false, true><<<p1_blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_kernel<L, false, false><<<p1_blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
-    }
+    launch_pass1(ld, info, n, flags, coeffs, ctl, qsub, qex, stats, stream);
     mark(HEXVAL_PHASE_PASS1, 1);
     mark(HEXVAL_PHASE_EXACT, 0);
-    const unsigned k5_blocks = (unsigned)info.sms * 4;
+    const unsigned k5_blocks = (unsigned)info.sms * 8;
     if (stats) exact_kernel<L, true><<<k5_blocks, K5_THREADS, 0, stream>>>(ld, flags, ctl, qex, qsub, stats);
     else exact_kernel<L, false><<<k5_blocks, K5_THREADS, 0, stream>>>(ld, flags, ctl, qex, qsub, stats);
     mark(HEXVAL_PHASE_EXACT, 1);
@@ -509,7 +848,6 @@ template <bool STATS>
 __global__ void __launch_bounds__(P1_THREADS) bezier_pass_kernel(const double* __restrict__ b, int64_t n,
                                                                  uint8_t* __restrict__ flags, Ctl* ctl,
                                                                  uint32_t* __restrict__ qsub, hexval_stats* stats) {
-    __shared__ unsigned int s_sub[33];
     const int64_t i = (int64_t)blockIdx.x * P1_THREADS + threadIdx.x;
     int st = -1;
     if (i < n) {
@@ -524,11 +862,11 @@ __global__ void __launch_bounds__(P1_THREADS) bezier_pass_kernel(const double* _
         st = !finite ? ST_NONFINITE : (m > 0 ? ST_VALID : ST_SUB);
         flags[i] = st == ST_NONFINITE ? HEXVAL_NONFINITE : (st == ST_VALID ? HEXVAL_VALID : HEXVAL_FLAG_SUBDIVIDED);
     }
-    block_append<P1_THREADS / 32>(st == ST_SUB, (uint32_t)i, qsub, &ctl->n_sub, s_sub);
+    warp_append(st == ST_SUB, (uint32_t)i, qsub, &ctl->n_sub);
     if (STATS) {
-        const int nv = __syncthreads_count(st == ST_VALID);
-        const int nn = __syncthreads_count(st == ST_NONFINITE);
-        if (threadIdx.x == 0) {
+        const unsigned nv = __popc(__ballot_sync(0xffffffffu, st == ST_VALID));
+        const unsigned nn = __popc(__ballot_sync(0xffffffffu, st == ST_NONFINITE));
+        if ((threadIdx.x & 31) == 0) {
             if (nv) atomicAdd(&stats->n_valid, (unsigned long long)nv);
             if (nn) atomicAdd(&stats->n_nonfinite, (unsigned long long)nn);
         }
@@ -540,22 +878,21 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return HEXVAL_ERR_CUDA;
     const DeviceInfo& info = device_info<SoaLoader>(dev);
-    const unsigned T = (unsigned)(info.sms * info.k4_blocks_per_sm * K4_THREADS);
+    const size_t warps = (size_t)info.sms * info.k4_blocks_per_sm * K4_WARPS;
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
-    const size_t fc_bytes = (size_t)MAX_DEPTH * 27 * T * sizeof(double);
-    const size_t fm_bytes = ((size_t)MAX_DEPTH * T + 255) & ~(size_t)255;
+    const size_t sc_bytes = warps * 27 * K4_CAP * sizeof(double);
+    const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
     char* base = nullptr;
-    if (cudaMallocAsync((void**)&base, ctl_bytes + q_bytes + fc_bytes + fm_bytes, stream) != cudaSuccess) {
+    if (cudaMallocAsync((void**)&base, ctl_bytes + q_bytes + sc_bytes + so_bytes, stream) != cudaSuccess) {
         cudaGetLastError();
         return HEXVAL_ERR_ALLOC;
     }
     Ctl* ctl = reinterpret_cast<Ctl*>(base);
     uint32_t* qsub = reinterpret_cast<uint32_t*>(base + ctl_bytes);
-    Frames fr;
+    WarpStacks fr;
     fr.coef = reinterpret_cast<double*>(base + ctl_bytes + q_bytes);
-    fr.mask = reinterpret_cast<unsigned char*>(base + ctl_bytes + q_bytes + fc_bytes);
-    fr.T = T;
+    fr.owner = reinterpret_cast<unsigned char*>(base + ctl_bytes + q_bytes + sc_bytes);
     cudaMemsetAsync(ctl, 0, ctl_bytes, stream);
     const unsigned p1_blocks = (unsigned)((n + P1_THREADS - 1) / P1_THREADS);
     if (stats) bezier_pass_kernel<true><<<p1_blocks, P1_THREADS, 0, stream>>>(b, n, flags, ctl, qsub, stats);

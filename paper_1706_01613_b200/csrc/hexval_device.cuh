@@ -203,93 +203,6 @@ __device__ __forceinline__ void root_coeffs(const Samples& s, const Coeffs& t, d
 }
 
 // ---------------------------------------------------------------------------
-// S7: de Casteljau subdivision at t = 1/2 ("as described
-// in [johnen2013]"; reading G3).  A line (p0, p1, p2) gives
-//   m01 = (p0+p1)/2, m12 = (p1+p2)/2, m = (m01+m12)/2
-//   left half (p0, m01, m), right half (m, m12, p2).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double half_sum(double a, double b) { return __dmul_rn(0.5, __dadd_rn(a, b)); }
-
-// Split all 9 lines of axis AX of a 3x3x3 node (P, layout i + 3j + 9k) into
-// a 5-point line each: G[slot(axis index 0..4, other two)].
-template <int AX>
-__device__ __forceinline__ int lin3(int a, int u, int w) {   // index in a 3x3x3 block, axis AX has index a
-    return AX == 0 ? a + 3 * u + 9 * w : (AX == 1 ? u + 3 * a + 9 * w : u + 3 * w + 9 * a);
-}
-
-// One half (h = 0 left, 1 right) of a node along axis AX, into Q (3x3x3).
-template <int AX>
-__device__ __forceinline__ void half_split(const double* P, int h, double* Q) {
-#pragma unroll
-    for (int u = 0; u < 3; ++u)
-#pragma unroll
-        for (int w = 0; w < 3; ++w) {
-            const double p0 = P[lin3<AX>(0, u, w)], p1 = P[lin3<AX>(1, u, w)], p2 = P[lin3<AX>(2, u, w)];
-            const double m01 = half_sum(p0, p1), m12 = half_sum(p1, p2), m = half_sum(m01, m12);
-            if (h == 0) {
-                Q[lin3<AX>(0, u, w)] = p0; Q[lin3<AX>(1, u, w)] = m01; Q[lin3<AX>(2, u, w)] = m;
-            } else {
-                Q[lin3<AX>(0, u, w)] = m; Q[lin3<AX>(1, u, w)] = m12; Q[lin3<AX>(2, u, w)] = p2;
-            }
-        }
-}
-
-// Both halves at once: G holds 5 points per line along AX (G[lin5]), the
-// left child is points 0..2 and the right child points 2..4.
-template <int AX>
-__device__ __forceinline__ int lin5(int a, int u, int w) {
-    return AX == 0 ? a + 5 * u + 15 * w : (AX == 1 ? u + 3 * a + 15 * w : u + 3 * w + 9 * a);
-}
-
-template <int AX>
-__device__ __forceinline__ void both_split(const double* P, double* G) {
-#pragma unroll
-    for (int u = 0; u < 3; ++u)
-#pragma unroll
-        for (int w = 0; w < 3; ++w) {
-            const double p0 = P[lin3<AX>(0, u, w)], p1 = P[lin3<AX>(1, u, w)], p2 = P[lin3<AX>(2, u, w)];
-            const double m01 = half_sum(p0, p1), m12 = half_sum(p1, p2), m = half_sum(m01, m12);
-            G[lin5<AX>(0, u, w)] = p0; G[lin5<AX>(1, u, w)] = m01; G[lin5<AX>(2, u, w)] = m;
-            G[lin5<AX>(3, u, w)] = m12; G[lin5<AX>(4, u, w)] = p2;
-        }
-}
-
-template <int AX>
-__device__ __forceinline__ void take_half(const double* G, int h, double* Q) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int u = 0; u < 3; ++u)
-#pragma unroll
-            for (int w = 0; w < 3; ++w) Q[lin3<AX>(a, u, w)] = G[lin5<AX>(2 * h + a, u, w)];
-}
-
-// Child (hx, hy, hz) of P, values bit-identical to those produced by the
-// both-halves path used for testing (same three operations per value).
-__device__ __forceinline__ void extract_child(const double* P, int hx, int hy, int hz, double* C) {
-    double A[27], B[27];
-    half_split<0>(P, hx, A);
-    half_split<1>(A, hy, B);
-    half_split<2>(B, hz, C);
-}
-
-// Classification of one child: returns 0 = some corner
-// coefficient <= 0 (False), 1 = all of b_9..27 > 0 (skip), 2 = undecided.
-__device__ __forceinline__ int classify_child(const double* C) {
-    int mc = key(C[0]);
-    mc = min(mc, key(C[2])); mc = min(mc, key(C[6])); mc = min(mc, key(C[8]));
-    mc = min(mc, key(C[18])); mc = min(mc, key(C[20])); mc = min(mc, key(C[24])); mc = min(mc, key(C[26]));
-    if (mc <= 0) return 0;
-    int mi = key(C[1]);
-    mi = min(mi, key(C[3])); mi = min(mi, key(C[4])); mi = min(mi, key(C[5])); mi = min(mi, key(C[7]));
-#pragma unroll
-    for (int q = 9; q < 18; ++q) mi = min(mi, key(C[q]));
-    mi = min(mi, key(C[19])); mi = min(mi, key(C[21])); mi = min(mi, key(C[22]));
-    mi = min(mi, key(C[23])); mi = min(mi, key(C[25]));
-    return mi > 0 ? 1 : 2;
-}
-
-// ---------------------------------------------------------------------------
 // K5: exact sign of one root sample, Kulisch-style long accumulator.
 // A sample is det(a, b, c) where every component of a, b, c is a signed sum of
 // 2 or 4 input coordinates, so det = sum of +-x*y*z over input doubles.  Each
@@ -418,7 +331,7 @@ __device__ __forceinline__ bool sample_has_zero_edge(const double* X, int j) {
 }
 
 // exact sign of sample j (0..19) of the hex with coordinates X
-__device__ int exact_sample_sign(const double* X, int j) {
+__device__ __noinline__ int exact_sample_sign(const double* X, int j) {
     if (sample_has_zero_edge(X, j)) return 0;
     uint64_t acc[KW];
 #pragma unroll 1

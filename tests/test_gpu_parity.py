@@ -8,6 +8,8 @@ configuration bench.py times; the oracle checks a sample of the outputs
 (random hexes plus every hex that took the exact-sign or subdivision path)
 and, for config 4, the closed-form verdict of every hex.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -131,6 +133,55 @@ def test_ragged_sizes_high_noise(n):
     assert_flags_match(f, ref, allow_near=True)
     assert ref["near"].sum() <= max(1, n // 5000)
     assert_coeffs_match(k, ref["coeffs"], f)
+
+
+@pytest.mark.parametrize("n", [256 * 148 * 4 + 1, 256 * 148 * 3, 256 * 300 + 255])
+def test_tma_pipeline_sizes(n):
+    """Several chunks per persistent warp, odd n (shifted plane copies) and a ragged tail."""
+    coords = hexgen.ragged_soa(n, seed=n % 1000, amp=0.45)
+    f, k = gpu_soa(coords, coeffs=True)
+    ref = oracle.check_soa(coords, want_coeffs=True)
+    assert_flags_match(f, ref, allow_near=True)
+    assert ref["near"].sum() <= max(1, n // 5000)
+    assert_coeffs_match(k, ref["coeffs"], f)
+
+
+def test_misaligned_base_uses_plain_path_with_same_results():
+    """An 8-B aligned (not 16-B) coordinate pointer takes the plain kernel: same bits."""
+    n = 5003
+    coords = hexgen.ragged_soa(n, seed=77, amp=0.45)
+    big = torch.empty(24 * n + 1, dtype=torch.float64, device="cuda")
+    big[1:] = torch.from_numpy(coords.ravel()).cuda()
+    view = big[1:].view(24, n)
+    assert view.data_ptr() % 16 == 8
+    f1, k1 = hv.check_soa(view, coeffs=True)
+    f2, k2 = gpu_soa(coords, coeffs=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(f1.cpu().numpy(), f2) and np.array_equal(k1.cpu().numpy(), k2)
+
+
+def test_pass1_variants_bit_identical(tmp_path):
+    """HEXVAL_PASS1=ldg|wtma (tuning knob) give identical flags and coefficients."""
+    import subprocess
+    import sys
+    n = 256 * 148 * 2 + 77
+    coords = hexgen.ragged_soa(n, seed=5, amp=0.5)
+    np.save(tmp_path / "c.npy", coords)
+    script = (
+        "import sys, numpy as np, torch\n"
+        f"sys.path.insert(0, {str(hexgen.__file__.rsplit('/', 2)[0])!r})\n"
+        "import paper_1706_01613_b200 as hv\n"
+        f"c = torch.from_numpy(np.load({str(tmp_path / 'c.npy')!r})).cuda()\n"
+        "f, k = hv.check_soa(c, coeffs=True); torch.cuda.synchronize()\n"
+        f"np.save({str(tmp_path)!r} + '/f_' + sys.argv[1] + '.npy', f.cpu().numpy())\n"
+        f"np.save({str(tmp_path)!r} + '/k_' + sys.argv[1] + '.npy', k.cpu().numpy())\n")
+    for v in ("ldg", "wtma"):
+        env = dict(os.environ, HEXVAL_PASS1=v)
+        subprocess.run([sys.executable, "-c", script, v], env=env, check=True, timeout=300)
+    f0, k0 = np.load(tmp_path / "f_ldg.npy"), np.load(tmp_path / "k_ldg.npy")
+    for v in ("wtma",):
+        assert np.array_equal(np.load(tmp_path / f"f_{v}.npy"), f0), v
+        assert np.array_equal(np.load(tmp_path / f"k_{v}.npy"), k0), v
 
 
 def test_subdivision_heavy_random_hexes():
@@ -281,3 +332,22 @@ def test_config4_full_size_closed_form_and_sampled():
     sel = np.unique(rng.choice(r.size, size=3000, replace=False))
     ref = oracle.check_soa(np.ascontiguousarray(coords[:, sel]))
     assert_flags_match(f[sel], ref)
+
+
+def test_subdivision_node_count_equals_oracle_for_valid_hexes():
+    """VALID hexes explore their whole capped tree, so the number of subdivided nodes is
+    order independent (reading G4): the warp-cooperative K4 must count exactly what the
+    oracle's depth-first recursion counts."""
+    coords, r = hexgen.adversarial_config(4000, seed=4, start=100_001)
+    ids = np.arange(100_001, 104_001)
+    sel = np.nonzero((ids % 2 == 1) & (r > 0))[0]           # twisted prisms, valid
+    c = np.ascontiguousarray(coords[:, sel])
+    ref = oracle.check_soa(c)
+    assert not ref["near"].any()
+    assert np.all(ref["flags"] == (hv.VALID | hv.FLAG_SUBDIVIDED))
+    stats = hv.Stats()
+    f, _ = gpu_soa(c, stats=stats)
+    assert np.array_equal(f, ref["flags"])
+    st = stats.read()
+    assert st["n_subdivided"] == sel.size
+    assert st["n_nodes"] == int(ref["nodes"].sum())
