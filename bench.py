@@ -67,7 +67,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
-    p.add_argument("--variant", choices=["ldg", "wtma"], default=None,
+    p.add_argument("--variant", choices=["ldg", "wtma", "cp"], default=None,
                    help="pass-1 kernel variant for SoA inputs (sets HEXVAL_PASS1; default: the library's)")
     args = p.parse_args()
     if args.variant:
@@ -162,19 +162,14 @@ def dist_setup(gpus: int):
 
 
 def dist_max(x: float, world: int) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_1706_01613_b200 import shard
+    return shard.max_over_ranks(x) if world > 1 else x
 
 
 def barrier(world: int):
+    from paper_1706_01613_b200 import shard
     if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+        shard.barrier()
 
 
 # ---------------------------------------------------------------------------
@@ -249,11 +244,12 @@ def run_reference(args, world, rank):
 def make_inputs(cfg: int, rank: int):
     """Host arrays of this rank's shard (weak scaling: every rank its own n hexes)."""
     import hexgen
-    n = hexgen.config_size(cfg)
+    from paper_1706_01613_b200 import shard
+    start, n = shard.weak_shard(hexgen.config_size(cfg), rank)
     if cfg in (0, 1):
-        return "soa", n, (hexgen.soa_config(n, 0.25 if cfg == 0 else 0.35, cfg, start=rank * n),)
+        return "soa", n, (hexgen.soa_config(n, 0.25 if cfg == 0 else 0.35, cfg, start=start),)
     if cfg == 4:
-        coords, _ = hexgen.adversarial_config(n, 4, start=rank * n)
+        coords, _ = hexgen.adversarial_config(n, 4, start=start)
         return "soa", n, (coords,)
     _, verts, idx = hexgen.make(cfg)
     return "indexed", n, (verts, idx)
@@ -291,6 +287,11 @@ def run_ours(args, world, rank, local):
     step(stats=stats)
     torch.cuda.synchronize()
     st = stats.read()
+    if world > 1:                                                      # whole-job verdict counts
+        from paper_1706_01613_b200 import shard
+        md = st["max_depth"]
+        st = dict(zip(st.keys(), shard.sum_over_ranks(list(st.values()))))
+        st["max_depth"] = int(shard.max_over_ranks(md))
 
     for _ in range(args.warmup):
         step()
@@ -335,7 +336,7 @@ def run_ours(args, world, rank, local):
         "timing": "CUDA events recorded by the library on the launching stream around each kernel, averaged over the timed steps",
     }
     subdivision = {
-        "rate": st["n_subdivided"] / n,
+        "rate": st["n_subdivided"] / (world * n),
         "nodes_per_step": st["n_nodes"],
         "subdiv_kernel_ms": subdiv_ms,
         "nodes_per_s": (st["n_nodes"] / (subdiv_ms * 1e-3)) if subdiv_ms > 0 and st["n_nodes"] else None,
@@ -393,7 +394,7 @@ def run_ours(args, world, rank, local):
             "gpu_launches": hv.kernel_launches_per_call() * args.steps,
             "clocks": clk.summary(),
             "subdivision": subdivision,
-            "subdivision_rate": st["n_subdivided"] / n,
+            "subdivision_rate": st["n_subdivided"] / (world * n),
             "verdicts": {"valid": st["n_valid"], "invalid": st["n_invalid"],
                          "undetermined": st["n_undetermined"], "nonfinite": st["n_nonfinite"],
                          "subdivided": st["n_subdivided"], "exact_sign_hexes": st["n_exact"],

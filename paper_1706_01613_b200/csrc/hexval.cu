@@ -268,12 +268,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "{\n"
         ".reg .pred P1;\n"
         "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@P1 bra DONE;\n"
         "bra LAB_WAIT;\n"
         "DONE:\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)                       // suspend-time hint (ns): sleep, do not spin
         : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
@@ -356,6 +356,130 @@ __global__ void __launch_bounds__(WT_THREADS, 2)
         }
         warp_epilogue<STATS>(st, i, ctl, qsub, qexact, stats);
     }
+}
+
+// ---------------------------------------------------------------------------
+// K1 (cp.async variant): persistent SoA pass 1.  Each thread prefetches the
+// 24 coordinates of its hex in the block's next 256-hex tile into its own
+// shared-memory slots with 8-byte async copies (LDGSTS) while it computes the
+// current tile; cp.async.wait_group blocks in hardware (no spinning) and no
+// block barrier is needed because every thread reads only what it copied.
+// ---------------------------------------------------------------------------
+constexpr int CP_THREADS = 256;
+constexpr size_t CP_SMEM = (size_t)2 * 24 * CP_THREADS * sizeof(double);   // 96 KB: two tiles
+
+__device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, uint64_t policy) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "l"(policy)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+__device__ __forceinline__ void cp_issue_hex(const double* __restrict__ coords, int64_t n, int64_t i, uint32_t dst) {
+    if (i < n) {
+        const uint64_t policy = policy_evict_first();
+#pragma unroll
+        for (int p = 0; p < 24; ++p) cp_async8(dst + p * CP_THREADS * 8, coords + (int64_t)p * n + i, policy);
+    }
+    cp_async_commit();                                        // (possibly empty) group per tile
+}
+
+template <bool COEFFS, bool STATS>
+__global__ void __launch_bounds__(CP_THREADS, 2)
+    pass1_soa_cp_kernel(const double* __restrict__ coords, int64_t n, uint8_t* __restrict__ flags,
+                        double* __restrict__ coeffs, Ctl* ctl, uint32_t* __restrict__ qsub,
+                        uint32_t* __restrict__ qexact, hexval_stats* stats) {
+    extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS]
+    const int tid = threadIdx.x;
+    const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
+    const uint32_t s0 = smem_u32(cp_buf + tid);
+    const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
+    int64_t t = blockIdx.x;
+    cp_issue_hex(coords, n, t * CP_THREADS + tid, s0);
+    cp_issue_hex(coords, n, (t + gridDim.x) * CP_THREADS + tid, s1);
+    for (int k = 0; t < tiles; t += gridDim.x, ++k) {
+        const int b = k & 1;
+        cp_async_wait1();                                    // tile k has landed (tile k+1 may be in flight)
+        const int64_t i = t * CP_THREADS + tid;
+        int st = -1;
+        if (i < n) {
+            const double* src = cp_buf + b * 24 * CP_THREADS + tid;
+            double X[24];
+#pragma unroll
+            for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
+            st = pass1_hex<COEFFS>(SoaLoader{coords, n}, X, i, n, flags, coeffs);
+        }
+        // refill this buffer with tile k+2 (X was consumed above: program order)
+        cp_issue_hex(coords, n, (t + 2 * (int64_t)gridDim.x) * CP_THREADS + tid, b ? s1 : s0);
+        warp_epilogue<STATS>(st, i, ctl, qsub, qexact, stats);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// K2 (cp.async variant): the same pipeline for int32 connectivity.  The 8
+// vertex ids of the thread's hex two tiles ahead are loaded into registers one
+// iteration early (their latency hides behind a whole tile of compute), then
+// the 24 coordinates are gathered into shared memory with async copies (L1
+// allocating: neighbouring hexes share vertices).
+__device__ __forceinline__ void load_idx8(const int32_t* __restrict__ idx, int64_t n, int64_t i, int4& a, int4& b) {
+    if (i < n) {
+        a = __ldcs(reinterpret_cast<const int4*>(idx) + 2 * i);
+        b = __ldcs(reinterpret_cast<const int4*>(idx) + 2 * i + 1);
+    }
+}
+
+__device__ __forceinline__ void cp_gather_hex(const double* __restrict__ verts, int64_t n, int64_t i, const int4& a,
+                                              const int4& b, uint32_t dst) {
+    if (i < n) {
+        const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        uint64_t policy;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(policy));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const double* src = verts + 3 * (int64_t)v[k];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) cp_async8(dst + (3 * k + ax) * CP_THREADS * 8, src + ax, policy);
+        }
+    }
+    cp_async_commit();
+}
+
+template <bool COEFFS, bool STATS>
+__global__ void __launch_bounds__(CP_THREADS, 2)
+    pass1_idx_cp_kernel(const double* __restrict__ verts, const int32_t* __restrict__ idx, int64_t n,
+                        uint8_t* __restrict__ flags, double* __restrict__ coeffs, Ctl* ctl,
+                        uint32_t* __restrict__ qsub, uint32_t* __restrict__ qexact, hexval_stats* stats) {
+    extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS]
+    const int tid = threadIdx.x;
+    const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
+    const int64_t G = gridDim.x;
+    const uint32_t s0 = smem_u32(cp_buf + tid);
+    const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
+    const IdxLoader ld{verts, idx};
+    int64_t t = blockIdx.x;
+    int4 a, b;
+    load_idx8(idx, n, t * CP_THREADS + tid, a, b);
+    cp_gather_hex(verts, n, t * CP_THREADS + tid, a, b, s0);
+    load_idx8(idx, n, (t + G) * CP_THREADS + tid, a, b);
+    cp_gather_hex(verts, n, (t + G) * CP_THREADS + tid, a, b, s1);
+    load_idx8(idx, n, (t + 2 * G) * CP_THREADS + tid, a, b);
+    for (int k = 0; t < tiles; t += G, ++k) {
+        const int bb = k & 1;
+        cp_async_wait1();
+        const int64_t i = t * CP_THREADS + tid;
+        int st = -1;
+        if (i < n) {
+            const double* src = cp_buf + bb * 24 * CP_THREADS + tid;
+            double X[24];
+#pragma unroll
+            for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
+            st = pass1_hex<COEFFS>(ld, X, i, n, flags, coeffs);
+        }
+        cp_gather_hex(verts, n, (t + 2 * G) * CP_THREADS + tid, a, b, bb ? s1 : s0);
+        load_idx8(idx, n, (t + 3 * G) * CP_THREADS + tid, a, b);
+        warp_epilogue<STATS>(st, i, ctl, qsub, qexact, stats);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -476,8 +600,8 @@ struct CoeffRoot {
     }
 };
 
-template <class R, bool STATS>
-__global__ void __launch_bounds__(K4_THREADS) subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
+template <class R, bool STATS, int MINB>
+__global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
                                                             const uint32_t* __restrict__ qsub, WarpStacks ws,
                                                             hexval_stats* stats) {
     __shared__ K4Warp wst[K4_WARPS];
@@ -660,7 +784,8 @@ __global__ void __launch_bounds__(K4_THREADS) subdiv_kernel(R root, uint8_t* __r
 struct DeviceInfo {
     int sms = 0;
     int k4_blocks_per_sm = 0;
-    bool p1_wtma = false;         // SoA pass 1: warp-TMA kernel (else the plain kernel)
+    int k4_minb = 2;
+    int p1_variant = 0;           // SoA pass 1: P1_LDG (plain), P1_WTMA or P1_CP
     int p1_ctas_per_sm = 1;
     bool ok = false;
 };
@@ -687,12 +812,34 @@ int wtma_setup() {
     return occ;
 }
 
-// Pass-1 variant for SoA inputs: HEXVAL_PASS1 = ldg | wtma (tuning knob for
-// measurements; default wtma when the device supports its shared memory).
+int cp_setup() {
+    const void* fns[8] = {(const void*)pass1_soa_cp_kernel<false, false>, (const void*)pass1_soa_cp_kernel<false, true>,
+                          (const void*)pass1_soa_cp_kernel<true, false>, (const void*)pass1_soa_cp_kernel<true, true>,
+                          (const void*)pass1_idx_cp_kernel<false, false>, (const void*)pass1_idx_cp_kernel<false, true>,
+                          (const void*)pass1_idx_cp_kernel<true, false>, (const void*)pass1_idx_cp_kernel<true, true>};
+    for (const void* f : fns)
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CP_SMEM) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass1_soa_cp_kernel<false, false>, CP_THREADS, CP_SMEM) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return occ;
+}
+
+// Pass-1 variant for SoA inputs: HEXVAL_PASS1 = ldg | wtma | cp (tuning knob
+// for measurements).
+enum { P1_LDG = 0, P1_WTMA = 1, P1_CP = 2 };
 int pass1_variant_from_env() {
     const char* v = getenv("HEXVAL_PASS1");
-    if (v && !strcmp(v, "ldg")) return 0;
-    return 1;
+    if (v && !strcmp(v, "wtma")) return P1_WTMA;
+    if (v && !strcmp(v, "cp")) return P1_CP;
+    if (v && !strcmp(v, "ldg")) return P1_LDG;
+    return P1_CP;                 // measured best on B200 (profiles/r01)
 }
 
 template <class L>
@@ -702,11 +849,18 @@ const DeviceInfo& device_info(int dev) {
     if (!d.ok) {
         cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false>, K4_THREADS, 0);
+        // K4 register budget: HEXVAL_K4_MINB = 2 (<= 255 regs, 8 warps/SM, no spills) or 3 (<= 168 regs,
+        // 12 warps/SM, small spills) -- tuning knob for measurements
+        const char* mb = getenv("HEXVAL_K4_MINB");
+        d.k4_minb = (mb && atoi(mb) == 3) ? 3 : 2;
+        if (d.k4_minb == 3)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false, 3>, K4_THREADS, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false, 2>, K4_THREADS, 0);
         d.k4_blocks_per_sm = occ > 0 ? occ : 1;
         const int want = pass1_variant_from_env();
-        const int ctas = want ? wtma_setup() : 0;
-        d.p1_wtma = ctas > 0;
+        const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup() : 0);
+        d.p1_variant = ctas > 0 ? want : P1_LDG;
         d.p1_ctas_per_sm = ctas > 0 ? ctas : 1;
         // keep freed stream-ordered scratch in the pool between calls
         cudaMemPool_t pool;
@@ -746,8 +900,29 @@ void launch_pass1_plain(const L& ld, int64_t n, uint8_t* flags, double* coeffs, 
 
 template <class L>
 void launch_pass1(const L& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl,
-                  uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
-    launch_pass1_plain(ld, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+                  uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream);
+
+// indexed: the cp.async gather pipeline when the connectivity rows are 16-B
+// aligned (int4 loads), else the plain kernel
+template <>
+void launch_pass1<IdxLoader>(const IdxLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs,
+                             Ctl* ctl, uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
+    if (info.p1_variant != P1_CP || (((uintptr_t)ld.idx) & 15) != 0) {
+        launch_pass1_plain(ld, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+        return;
+    }
+    const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
+    const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
+    const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+    const double* v = ld.verts;
+    const int32_t* x = ld.idx;
+    if (coeffs) {
+        if (stats) pass1_idx_cp_kernel<true, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_idx_cp_kernel<true, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+    } else {
+        if (stats) pass1_idx_cp_kernel<false, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_idx_cp_kernel<false, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+    }
 }
 
 void launch_wtma(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl,
@@ -766,15 +941,42 @@ void launch_wtma(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t
     }
 }
 
-// SoA: the warp-TMA kernel when the coordinate array is 16-B aligned (bulk
-// copies need it), else the plain kernel.
+void launch_cp(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl,
+               uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
+    const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
+    const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
+    const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+    const double* c = ld.coords;
+    if (coeffs) {
+        if (stats) pass1_soa_cp_kernel<true, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_soa_cp_kernel<true, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+    } else {
+        if (stats) pass1_soa_cp_kernel<false, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_soa_cp_kernel<false, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+    }
+}
+
+// SoA: the selected variant (warp-TMA needs a 16-B aligned coordinate array).
 template <>
 void launch_pass1<SoaLoader>(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags,
                              double* coeffs, Ctl* ctl, uint32_t* qsub, uint32_t* qex, hexval_stats* stats,
                              cudaStream_t stream) {
     const bool aligned = (((uintptr_t)ld.coords) & 15) == 0;
-    if (aligned && info.p1_wtma) launch_wtma(ld, info, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+    if (aligned && info.p1_variant == P1_WTMA) launch_wtma(ld, info, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+    else if (info.p1_variant == P1_CP) launch_cp(ld, info, n, flags, coeffs, ctl, qsub, qex, stats, stream);
     else launch_pass1_plain(ld, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+}
+
+template <class R>
+void launch_subdiv(const R& root, const DeviceInfo& info, unsigned blocks, uint8_t* flags, Ctl* ctl,
+                   const uint32_t* qsub, const WarpStacks& fr, hexval_stats* stats, cudaStream_t stream) {
+    if (info.k4_minb == 3) {
+        if (stats) subdiv_kernel<R, true, 3><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
+        else subdiv_kernel<R, false, 3><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
+    } else {
+        if (stats) subdiv_kernel<R, true, 2><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
+        else subdiv_kernel<R, false, 2><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
+    }
 }
 
 int collect_profile(hexval_profile* p) {
@@ -833,8 +1035,7 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     mark(HEXVAL_PHASE_SUBDIV, 0);
     const unsigned k4_blocks = (unsigned)(info.sms * info.k4_blocks_per_sm);
     const CoordRoot<L> root{ld};
-    if (stats) subdiv_kernel<CoordRoot<L>, true><<<k4_blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
-    else subdiv_kernel<CoordRoot<L>, false><<<k4_blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
+    launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, fr, stats, stream);
     mark(HEXVAL_PHASE_SUBDIV, 1);
     cudaFreeAsync(base, stream);
     if (cudaGetLastError() != cudaSuccess) return HEXVAL_ERR_CUDA;
@@ -899,8 +1100,7 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     else bezier_pass_kernel<false><<<p1_blocks, P1_THREADS, 0, stream>>>(b, n, flags, ctl, qsub, stats);
     const CoeffRoot root{b, n};
     const unsigned k4_blocks = (unsigned)(info.sms * info.k4_blocks_per_sm);
-    if (stats) subdiv_kernel<CoeffRoot, true><<<k4_blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
-    else subdiv_kernel<CoeffRoot, false><<<k4_blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
+    launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, fr, stats, stream);
     cudaFreeAsync(base, stream);
     if (cudaGetLastError() != cudaSuccess) return HEXVAL_ERR_CUDA;
     return HEXVAL_OK;
