@@ -67,6 +67,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
+    p.add_argument("--op", choices=["check", "quality"], default="check",
+                   help="check: the hot path (headline); quality: NEXT-2 corner screening kernel")
     p.add_argument("--variant", choices=["ldg", "wtma", "cp"], default=None,
                    help="pass-1 kernel variant for SoA inputs (sets HEXVAL_PASS1; default: the library's)")
     args = p.parse_args()
@@ -405,12 +407,65 @@ def run_ours(args, world, rank, local):
     return 0
 
 
+def run_op(args, world, rank, local):
+    """Secondary measurements of the NEXT rows: one kernel per step,
+    timed with CUDA events on the launching stream; roofline against HBM."""
+    import torch
+
+    import paper_1706_01613_b200 as hv
+
+    torch.cuda.set_device(local)
+    cfg = args.config
+    layout, n, host = make_inputs(cfg, rank)
+    dev = [torch.from_numpy(a).cuda() for a in host]
+    stream = torch.cuda.current_stream()
+    if args.op == "quality":
+        sj = torch.empty(n, dtype=torch.float64, device="cuda")
+        t1 = torch.empty(n, dtype=torch.uint8, device="cuda")
+
+        def step():
+            if layout == "soa":
+                hv.corner_quality_soa(dev[0], sj, t1)
+            else:
+                hv.corner_quality_indexed(dev[0], dev[1], sj, t1)
+        out_bytes = 9
+        metric = "hexahedra screened/sec (corner scaled Jacobian + Test 1, fp64, 1 B200)"
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = dist_max(ev0.elapsed_time(ev1) / args.steps, world)
+    algo = (192 * n if layout == "soa" else 32 * n + 24 * host[0].shape[0]) + out_bytes * n
+    peak, peak_src = measured_peaks()
+    ach = algo / (ms * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "op": args.op, "metric": metric, "value": world * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "ms_per_step": ms, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_DESC[cfg], "layout": layout, "n_hexes_per_rank": n},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": algo},
+            "gpu_launches": args.steps, "clocks": clk.summary()}), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     world, rank, local = dist_setup(args.gpus)
     try:
         if args.impl == "reference":
             return run_reference(args, world, rank)
+        if args.op != "check":
+            return run_op(args, world, rank, local)
         return run_ours(args, world, rank, local)
     finally:
         if world > 1:

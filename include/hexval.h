@@ -122,6 +122,22 @@ int hexval_check_indexed_ex(const double* vertices, const int32_t* hex_idx, int6
 int hexval_classify_bezier(const double* coeffs, int64_t n, uint8_t* flags_out,
                            hexval_stats* stats_dev_opt, cudaStream_t stream);
 
+/* ---- NEXT-2: screening by-products of the 8 corner samples ---------------------
+ * For every hex (layouts as above; outputs are device memory, either may be NULL):
+ *   sj_min_out_opt[i]  min over the 8 corners of the scaled Jacobian
+ *                      det J / (|d_xi x| |d_eta x| |d_zeta x|) at the corner -- the
+ *                      quality measure of PAPER.md:1212-1217 (Fig. 7: 0.64); NaN when a
+ *                      corner edge has zero length or the hex is NONFINITE;
+ *   test1_out_opt[i]   1 iff det J > 0 at all 8 corners (Ushakova's Test 1, the 8 corner
+ *                      tetrahedra: a necessary condition only, PAPER.md:107-109,
+ *                      1260-1263), fp64 sign of the corner sample.
+ * Asynchronous on `stream`; returns HEXVAL_OK or a negative status.              */
+int hexval_corner_quality_soa(const double* coords, int64_t n, double* sj_min_out_opt,
+                              uint8_t* test1_out_opt, cudaStream_t stream);
+int hexval_corner_quality_indexed(const double* vertices, const int32_t* hex_idx, int64_t n,
+                                  double* sj_min_out_opt, uint8_t* test1_out_opt,
+                                  cudaStream_t stream);
+
 /* ---- host-resident calls (synchronous, end to end) --------------------------
  * Same layouts, but every pointer is HOST memory (pinned memory gives
  * overlapped copies; pageable memory works but serialises).  The library

@@ -95,6 +95,11 @@ def lib():
         L.oracle_node_xi.argtypes = [ctypes.c_int, _D]
         L.oracle_classify_coeffs.argtypes = [_D, ctypes.c_double, ctypes.POINTER(OracleResult)]
         L.oracle_classify_coeffs.restype = ctypes.c_int
+        L.oracle_corner_quality.argtypes = [_D, _D, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+        L.oracle_corner_quality.restype = None
+        L.oracle_corner_quality_soa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                                ctypes.c_void_p, ctypes.c_int]
+        L.oracle_corner_quality_soa.restype = None
         L.oracle_num_threads.argtypes = [ctypes.c_int]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
@@ -214,3 +219,23 @@ def check_indexed(vertices: np.ndarray, hex_idx: np.ndarray, want_coeffs: bool =
     if coeffs is not None:
         out["coeffs"] = coeffs
     return out
+
+
+def corner_quality(X) -> dict:
+    """NEXT-2: min corner scaled Jacobian, Ushakova Test 1 (exact signs), near-zero flag."""
+    X = _hex(X)
+    sj = ctypes.c_double()
+    t1, nr = ctypes.c_int(), ctypes.c_int()
+    lib().oracle_corner_quality(_dptr(X), ctypes.byref(sj), ctypes.byref(t1), ctypes.byref(nr))
+    return {"sj_min": sj.value, "test1": t1.value, "near": nr.value}
+
+
+def corner_quality_soa(coords: np.ndarray, nthreads: int = 0) -> dict:
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    n = coords.shape[1]
+    sj = np.zeros(n)
+    t1 = np.zeros(n, np.uint8)
+    nr = np.zeros(n, np.uint8)
+    lib().oracle_corner_quality_soa(coords.ctypes.data, n, sj.ctypes.data, t1.ctypes.data, nr.ctypes.data,
+                                    int(nthreads))
+    return {"sj_min": sj, "test1": t1, "near": nr}

@@ -672,3 +672,59 @@ void oracle_check_indexed(const double* vertices, const int32_t* hex_idx, int64_
         store_one(&r, i, n, flags_out, coeffs_out, near_out, nodes_out, exact_out);
     }
 }
+
+/* -------------------------------------------------------------------------
+ * NEXT-2: corner screening quantities.
+ * At corner sigma (0..7) the Jacobian columns are the three edge vectors
+ * leaving the corner; the scaled Jacobian divides det J by
+ * the product of their lengths.
+ * ---------------------------------------------------------------------- */
+void oracle_corner_quality(const double X[8][3], double* sj_min, int* test1, int* near) {
+    for (int k = 0; k < 8; ++k)
+        for (int a = 0; a < 3; ++a)
+            if (!coord_ok(X[k][a])) {             /* NONFINITE input (reading G13) */
+                *sj_min = NAN;
+                *test1 = 0;
+                *near = 0;
+                return;
+            }
+    edges_t E;
+    edge_vectors(X, &E);
+    double m = INFINITY;
+    int all_pos = 1, nr = 0, undefined = 0;
+    for (int k = 0; k < 8; ++k) {
+        double xi[3], J[3][3], Ja[3][3];
+        oracle_node_xi(k, xi);
+        derivatives(&E, xi, J, Ja);
+        const double d = det_eps(J);
+        const double tau = 32.0 * U_ROUND * permanent_abs(Ja) + ldexp(1.0, -1060);
+        if (fabs(d) <= tau) nr = 1;
+        if (oracle_exact_sign(X, k) <= 0) all_pos = 0;
+        double len[3];
+        for (int r = 0; r < 3; ++r) len[r] = sqrt(J[r][0] * J[r][0] + J[r][1] * J[r][1] + J[r][2] * J[r][2]);
+        if (len[0] == 0.0 || len[1] == 0.0 || len[2] == 0.0) undefined = 1;
+        const double sj = d / (len[0] * len[1] * len[2]);
+        if (sj < m) m = sj;
+    }
+    *sj_min = undefined ? NAN : m;
+    *test1 = all_pos;
+    *near = nr;
+}
+
+void oracle_corner_quality_soa(const double* coords, int64_t n, double* sj_out, uint8_t* test1_out,
+                               uint8_t* near_out, int nthreads) {
+    const int nt = oracle_num_threads(nthreads);
+    (void)nt;
+#pragma omp parallel for schedule(dynamic, 256) num_threads(nt)
+    for (int64_t i = 0; i < n; ++i) {
+        double X[8][3];
+        for (int k = 0; k < 8; ++k)
+            for (int a = 0; a < 3; ++a) X[k][a] = coords[(int64_t)(3 * k + a) * n + i];
+        double sj;
+        int t1, nr;
+        oracle_corner_quality(X, &sj, &t1, &nr);
+        if (sj_out) sj_out[i] = sj;
+        if (test1_out) test1_out[i] = (uint8_t)t1;
+        if (near_out) near_out[i] = (uint8_t)nr;
+    }
+}

@@ -71,6 +71,18 @@ int    oracle_num_threads(int nthreads);
 /* Steps 4-5 on a given coefficient vector; E sets tau. */
 int    oracle_classify_coeffs(const double b[27], double E, oracle_result* r);
 
+/* NEXT-2, screening by-products of the 8 corner samples:
+ *   sj_min  min over the 8 corners of the scaled Jacobian det J / (|d_xi x| |d_eta x| |d_zeta x|)
+ *           at the corner (Fig. 7 caption "0.64"); NaN if a corner edge
+ *           has zero length (the metric is undefined there, SPEC.md baselines);
+ *   test1   1 iff det J > 0 at all 8 corners (Ushakova Test 1, the 8 corner tetrahedra,
+ *           PAPER.md:107-109, 1260-1263), each sign decided exactly;
+ *   near    1 iff some corner det J is within its fp64 rounding bound of 0.
+ * A NONFINITE hex (reading G13) gives sj_min = NaN, test1 = 0. */
+void   oracle_corner_quality(const double X[8][3], double* sj_min, int* test1, int* near);
+void   oracle_corner_quality_soa(const double* coords, int64_t n, double* sj_out, uint8_t* test1_out,
+                                 uint8_t* near_out, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ __all__ = [
     "INVALID", "VALID", "UNDETERMINED", "NONFINITE", "FLAG_SUBDIVIDED", "MAX_DEPTH",
     "HexvalError", "lib", "library_path", "check_soa", "check_indexed", "check_soa_host",
     "check_indexed_host", "classify_bezier", "Stats", "Profile", "status_string", "version",
-    "kernel_launches_per_call",
+    "kernel_launches_per_call", "corner_quality_soa", "corner_quality_indexed",
 ]
 
 INVALID, VALID, UNDETERMINED, NONFINITE = 0, 1, 2, 3
@@ -32,7 +32,8 @@ MAX_DEPTH = 20
 PHASES = ("pass1", "exact", "subdiv")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libhexval.so")
+# HEXVAL_LIB selects an in-tree variant build (A/B measurements); default libhexval.so
+_LIB_PATH = os.path.join(_HERE, os.environ.get("HEXVAL_LIB", "libhexval.so"))
 
 
 class HexvalError(RuntimeError):
@@ -64,6 +65,10 @@ def _load() -> ctypes.CDLL:
               "hexval_check_soa_host", "hexval_check_indexed_host", "hexval_version",
               "hexval_kernel_launches_per_call"):
         getattr(L, f).restype = ctypes.c_int
+    L.hexval_corner_quality_soa.argtypes = [_vp, _i64, _vp, _vp, _vp]
+    L.hexval_corner_quality_indexed.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp]
+    L.hexval_corner_quality_soa.restype = ctypes.c_int
+    L.hexval_corner_quality_indexed.restype = ctypes.c_int
     L.hexval_status_string.argtypes = [ctypes.c_int]
     L.hexval_status_string.restype = ctypes.c_char_p
     L.hexval_profile_create.argtypes = []
@@ -292,3 +297,40 @@ def check_indexed_host(vertices, hex_idx, flags, coeffs=None, chunk_hexes: int =
                                          _stream_handle(stream) if stream is not None else 0)
     _check(rc, "hexval_check_indexed_host")
     return flags
+
+
+def _quality_outputs(n, device, sj_min, test1):
+    torch = _torch()
+    if sj_min is None or sj_min is True:
+        sj_min = torch.empty(n, dtype=torch.float64, device=device)
+    if test1 is None or test1 is True:
+        test1 = torch.empty(n, dtype=torch.uint8, device=device)
+    _require(sj_min, torch.float64, "sj_min")
+    _require(test1, torch.uint8, "test1")
+    return sj_min, test1
+
+
+def corner_quality_soa(coords, sj_min=None, test1=None, stream=None):
+    """hexval_corner_quality_soa (NEXT-2): min corner scaled Jacobian and Ushakova Test 1 per hex."""
+    torch = _torch()
+    _require(coords, torch.float64, "coords", 2)
+    if coords.shape[0] != 24:
+        raise ValueError("coords must have shape (24, n)")
+    n = coords.shape[1]
+    sj_min, test1 = _quality_outputs(n, coords.device, sj_min, test1)
+    _check(lib().hexval_corner_quality_soa(coords.data_ptr(), n, sj_min.data_ptr(), test1.data_ptr(),
+                                           _stream_handle(stream)), "hexval_corner_quality_soa")
+    return sj_min, test1
+
+
+def corner_quality_indexed(vertices, hex_idx, sj_min=None, test1=None, stream=None):
+    """hexval_corner_quality_indexed (NEXT-2) on (nv, 3) float64 vertices and (n, 8) int32 connectivity."""
+    torch = _torch()
+    _require(vertices, torch.float64, "vertices", 2)
+    _require(hex_idx, torch.int32, "hex_idx", 2)
+    n = hex_idx.shape[0]
+    sj_min, test1 = _quality_outputs(n, hex_idx.device, sj_min, test1)
+    _check(lib().hexval_corner_quality_indexed(vertices.data_ptr(), hex_idx.data_ptr(), n, sj_min.data_ptr(),
+                                               test1.data_ptr(), _stream_handle(stream)),
+           "hexval_corner_quality_indexed")
+    return sj_min, test1

@@ -90,10 +90,19 @@ struct IdxLoader {
 
 // NONFINITE (reading G13): a coordinate is NaN/Inf or |x| > 2^300
 __device__ __forceinline__ bool out_of_range(const double* X) {
+#ifdef HEXVAL_KEYS_V2
+    // max |hi word| without masking: signed max covers x >= 0, unsigned max x < 0
+    int sm = 0x80000000;
+    unsigned um = 0;
+#pragma unroll
+    for (int p = 0; p < 24; ++p) { sm = max(sm, key(X[p])); um = max(um, (unsigned)key(X[p])); }
+    if (sm < 0x52B00000 && um < 0xD2B00000u) return false;   // every |x| < 2^300
+#else
     int mk = 0;
 #pragma unroll
     for (int p = 0; p < 24; ++p) mk = max(mk, abskey(X[p]));
     if (mk < 0x52B00000) return false;                 // every |x| < 2^300
+#endif
     bool bad = false;
 #pragma unroll
     for (int p = 0; p < 24; ++p) bad |= !(fabs(X[p]) <= 0x1p300);
@@ -135,19 +144,33 @@ __device__ __forceinline__ bool IdxLoader::dup_face_pair(int64_t i) const {
 enum : int { ST_INVALID = 0, ST_VALID = 1, ST_NONFINITE = 3, ST_SUB = 4, ST_EXACT = 5 };
 
 __device__ __forceinline__ int step2_class(const Samples& s, double tau2) {
+    const int T = key(tau2);                          // tau2 > 0: key == abskey
     int km = key(s.c[0]);
 #pragma unroll
     for (int k = 1; k < 8; ++k) km = min(km, key(s.c[k]));
 #pragma unroll
     for (int e = 0; e < 12; ++e) km = min(km, key(s.d[e]));
-    if (km > key(tau2)) return ST_VALID;               // every sample > tau2 > 0: robustly positive
+    if (km > T) return ST_VALID;                       // every sample > tau2 > 0: robustly positive
+#ifdef HEXVAL_STEP2_FP
     bool neg = false, amb = false;
 #pragma unroll
     for (int k = 0; k < 8; ++k) { neg |= s.c[k] < -tau2; amb |= fabs(s.c[k]) <= tau2; }
 #pragma unroll
     for (int e = 0; e < 12; ++e) { neg |= s.d[e] < -tau2; amb |= fabs(s.d[e]) <= tau2; }
-    if (neg) return ST_INVALID;                        // some sample robustly negative
+    if (neg) return ST_INVALID;
     return amb ? ST_EXACT : ST_VALID;
+#endif
+    // Slow path on the integer pipe, conservative in the hi words: a sample is
+    // robustly negative if its sign is set and its hi word exceeds that of
+    // tau2 (then |x| > tau2); it is ambiguous if |x|'s hi word <= that of tau2.
+    unsigned um = 0;
+    int am = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { um = max(um, (unsigned)key(s.c[k])); am = min(am, abskey(s.c[k])); }
+#pragma unroll
+    for (int e = 0; e < 12; ++e) { um = max(um, (unsigned)key(s.d[e])); am = min(am, abskey(s.d[e])); }
+    if (um > (0x80000000u | (unsigned)T)) return ST_INVALID;   // some sample robustly negative
+    return am <= T ? ST_EXACT : ST_VALID;
 }
 
 __device__ __forceinline__ void write_coeffs(double* __restrict__ coeffs, int64_t n, int64_t i,
@@ -169,6 +192,25 @@ __device__ __forceinline__ void warp_append(bool pred, uint32_t val, uint32_t* _
     base = __shfl_sync(0xffffffffu, base, leader);
     if (pred) q[base + __popc(bal & ((1u << lane) - 1u))] = val;
 }
+
+// Per-thread verdict counters of a persistent kernel, flushed once per warp.
+struct P1Counts {
+    unsigned v = 0, i = 0, n = 0;
+    __device__ __forceinline__ void add(int st) { v += st == ST_VALID; i += st == ST_INVALID; n += st == ST_NONFINITE; }
+    __device__ __forceinline__ void flush(hexval_stats* stats) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            v += __shfl_xor_sync(0xffffffffu, v, o);
+            i += __shfl_xor_sync(0xffffffffu, i, o);
+            n += __shfl_xor_sync(0xffffffffu, n, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (v) atomicAdd(&stats->n_valid, (unsigned long long)v);
+            if (i) atomicAdd(&stats->n_invalid, (unsigned long long)i);
+            if (n) atomicAdd(&stats->n_nonfinite, (unsigned long long)n);
+        }
+    }
+};
 
 template <bool STATS>
 __device__ __forceinline__ void warp_epilogue(int st, int64_t i, Ctl* ctl, uint32_t* __restrict__ qsub,
@@ -394,6 +436,7 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
     const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
     const uint32_t s0 = smem_u32(cp_buf + tid);
     const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
+    P1Counts cnt;
     int64_t t = blockIdx.x;
     cp_issue_hex(coords, n, t * CP_THREADS + tid, s0);
     cp_issue_hex(coords, n, (t + gridDim.x) * CP_THREADS + tid, s1);
@@ -411,9 +454,11 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
         }
         // refill this buffer with tile k+2 (X was consumed above: program order)
         cp_issue_hex(coords, n, (t + 2 * (int64_t)gridDim.x) * CP_THREADS + tid, b ? s1 : s0);
-        warp_epilogue<STATS>(st, i, ctl, qsub, qexact, stats);
+        warp_epilogue<false>(st, i, ctl, qsub, qexact, stats);
+        if (STATS) cnt.add(st);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (STATS) cnt.flush(stats);
 }
 
 // K2 (cp.async variant): the same pipeline for int32 connectivity.  The 8
@@ -456,6 +501,7 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
     const uint32_t s0 = smem_u32(cp_buf + tid);
     const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
     const IdxLoader ld{verts, idx};
+    P1Counts cnt;
     int64_t t = blockIdx.x;
     int4 a, b;
     load_idx8(idx, n, t * CP_THREADS + tid, a, b);
@@ -477,9 +523,65 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
         }
         cp_gather_hex(verts, n, (t + 2 * G) * CP_THREADS + tid, a, b, bb ? s1 : s0);
         load_idx8(idx, n, (t + 3 * G) * CP_THREADS + tid, a, b);
-        warp_epilogue<STATS>(st, i, ctl, qsub, qexact, stats);
+        warp_epilogue<false>(st, i, ctl, qsub, qexact, stats);
+        if (STATS) cnt.add(st);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (STATS) cnt.flush(stats);
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-2: screening by-products of the 8 corner samples:
+// the minimum corner scaled Jacobian det J / (|d_xi x||d_eta x||d_zeta x|)
+// and Ushakova's Test 1 -- det J > 0 at all 8 corners
+// (PAPER.md:107-109, 1260-1263).  One hex per thread, streaming; the argmin
+// over the corners compares c|c|/P by cross-multiplication (P = product of the
+// squared edge lengths), so only the winner takes a division and a sqrt.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double len2(const V3& v) {
+    return __fma_rn(v.z, v.z, __fma_rn(v.y, v.y, __dmul_rn(v.x, v.x)));
+}
+
+template <class L>
+__global__ void __launch_bounds__(256) quality_kernel(L ld, int64_t n, double* __restrict__ sj_out,
+                                                       uint8_t* __restrict__ t1_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double X[24];
+    ld.load_stream(i, X);
+    double sj = __longlong_as_double(0x7ff8000000000000ll);   // NaN: undefined / NONFINITE
+    uint8_t t1 = 0;
+    if (!out_of_range(X)) {
+        const V3 n1{X[0], X[1], X[2]}, n2{X[3], X[4], X[5]}, n3{X[6], X[7], X[8]}, n4{X[9], X[10], X[11]};
+        const V3 n5{X[12], X[13], X[14]}, n6{X[15], X[16], X[17]}, n7{X[18], X[19], X[20]}, n8{X[21], X[22], X[23]};
+        const V3 v12 = vsub(n2, n1), v43 = vsub(n3, n4), v56 = vsub(n6, n5), v87 = vsub(n7, n8);
+        const V3 v14 = vsub(n4, n1), v23 = vsub(n3, n2), v58 = vsub(n8, n5), v67 = vsub(n7, n6);
+        const V3 v15 = vsub(n5, n1), v26 = vsub(n6, n2), v48 = vsub(n8, n4), v37 = vsub(n7, n3);
+        // corner k: (d_xi, d_eta, d_zeta) = the three edges leaving it
+        const double c[8] = {det3(v12, v14, v15), det3(v12, v23, v26), det3(v43, v23, v37), det3(v43, v14, v48),
+                             det3(v56, v58, v15), det3(v56, v67, v26), det3(v87, v67, v37), det3(v87, v58, v48)};
+        const double l12 = len2(v12), l43 = len2(v43), l56 = len2(v56), l87 = len2(v87);
+        const double l14 = len2(v14), l23 = len2(v23), l58 = len2(v58), l67 = len2(v67);
+        const double l15 = len2(v15), l26 = len2(v26), l48 = len2(v48), l37 = len2(v37);
+        const double P[8] = {__dmul_rn(__dmul_rn(l12, l14), l15), __dmul_rn(__dmul_rn(l12, l23), l26),
+                             __dmul_rn(__dmul_rn(l43, l23), l37), __dmul_rn(__dmul_rn(l43, l14), l48),
+                             __dmul_rn(__dmul_rn(l56, l58), l15), __dmul_rn(__dmul_rn(l56, l67), l26),
+                             __dmul_rn(__dmul_rn(l87, l67), l37), __dmul_rn(__dmul_rn(l87, l58), l48)};
+        int km = key(c[0]);
+        double bn = __dmul_rn(c[0], fabs(c[0])), bp = P[0];
+        bool zero_edge = !(P[0] > 0.0);
+#pragma unroll
+        for (int k = 1; k < 8; ++k) {
+            km = min(km, key(c[k]));
+            zero_edge |= !(P[k] > 0.0);
+            const double nk = __dmul_rn(c[k], fabs(c[k]));
+            if (__dmul_rn(nk, bp) < __dmul_rn(bn, P[k])) { bn = nk; bp = P[k]; }   // nk/P[k] < bn/bp
+        }
+        t1 = km > 0;
+        if (!zero_edge) sj = copysign(sqrt(__ddiv_rn(fabs(bn), bp)), bn);
+    }
+    if (sj_out) __stcs(sj_out + i, sj);
+    if (t1_out) __stcs(t1_out + i, t1);
 }
 
 // ---------------------------------------------------------------------------
@@ -491,7 +593,7 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
 __device__ __noinline__ uint8_t exact_resolve(const double* X) {
     Samples s;
     samples20(X, s);
-    const double tau2 = step2_tau(s.ekey);
+    const int T = key(step2_tau(s.ekey));
     double v[20];
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = s.c[j];
@@ -499,8 +601,8 @@ __device__ __noinline__ uint8_t exact_resolve(const double* X) {
     for (int e = 0; e < 12; ++e) v[8 + e] = s.d[e];
 #pragma unroll 1
     for (int j = 0; j < 20; ++j) {
-        if (v[j] < -tau2) return HEXVAL_INVALID;
-        if (fabs(v[j]) <= tau2 && exact_sample_sign(X, j) <= 0) return HEXVAL_INVALID;
+        if ((unsigned)key(v[j]) > (0x80000000u | (unsigned)T)) return HEXVAL_INVALID;   // robustly negative
+        if (abskey(v[j]) <= T && exact_sample_sign(X, j) <= 0) return HEXVAL_INVALID;   // exact sign
     }
     Coeffs t;
     transform(s, t);
@@ -1141,6 +1243,28 @@ int hexval_classify_bezier(const double* coeffs, int64_t n, uint8_t* flags_out, 
     if (n > 0 && (!coeffs || !flags_out)) return HEXVAL_ERR_ARGUMENT;
     if (misaligned(coeffs, 8) || misaligned(stats_dev_opt, 8)) return HEXVAL_ERR_ALIGNMENT;
     return run_bezier(coeffs, n, flags_out, stats_dev_opt, stream);
+}
+
+int hexval_corner_quality_soa(const double* coords, int64_t n, double* sj_min_out_opt, uint8_t* test1_out_opt,
+                              cudaStream_t stream) {
+    if (n < 0 || n > INT32_MAX) return HEXVAL_ERR_ARGUMENT;
+    if (n > 0 && !coords) return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(coords, 8) || misaligned(sj_min_out_opt, 8)) return HEXVAL_ERR_ALIGNMENT;
+    if (n == 0) return HEXVAL_OK;
+    quality_kernel<SoaLoader><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(SoaLoader{coords, n}, n, sj_min_out_opt,
+                                                                               test1_out_opt);
+    return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
+}
+
+int hexval_corner_quality_indexed(const double* vertices, const int32_t* hex_idx, int64_t n, double* sj_min_out_opt,
+                                  uint8_t* test1_out_opt, cudaStream_t stream) {
+    if (n < 0 || n > INT32_MAX) return HEXVAL_ERR_ARGUMENT;
+    if (n > 0 && (!vertices || !hex_idx)) return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(vertices, 8) || misaligned(hex_idx, 4) || misaligned(sj_min_out_opt, 8)) return HEXVAL_ERR_ALIGNMENT;
+    if (n == 0) return HEXVAL_OK;
+    quality_kernel<IdxLoader><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(IdxLoader{vertices, hex_idx}, n,
+                                                                               sj_min_out_opt, test1_out_opt);
+    return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
 }
 
 int hexval_check_soa(const double* coords, int64_t n, uint8_t* flags_out, double* coeffs_out_opt,

@@ -66,6 +66,19 @@ __device__ __forceinline__ void samples20(const double* X, Samples& s) {
     const V3 v12 = vsub(n2, n1), v43 = vsub(n3, n4), v56 = vsub(n6, n5), v87 = vsub(n7, n8);
     const V3 v14 = vsub(n4, n1), v23 = vsub(n3, n2), v58 = vsub(n8, n5), v67 = vsub(n7, n6);
     const V3 v15 = vsub(n5, n1), v26 = vsub(n6, n2), v48 = vsub(n8, n4), v37 = vsub(n7, n3);
+#ifdef HEXVAL_KEYS_V2
+    // max |hi word| of the 36 components: signed max covers components >= 0,
+    // unsigned max (sign bit set = largest) covers negative ones
+    int sm = 0x80000000;
+    unsigned um = 0;
+#define HV_EK(v) sm = max(sm, max(key(v.x), max(key(v.y), key(v.z)))); \
+                 um = max(um, max((unsigned)key(v.x), max((unsigned)key(v.y), (unsigned)key(v.z))))
+    HV_EK(v12); HV_EK(v43); HV_EK(v56); HV_EK(v87);
+    HV_EK(v14); HV_EK(v23); HV_EK(v58); HV_EK(v67);
+    HV_EK(v15); HV_EK(v26); HV_EK(v48); HV_EK(v37);
+#undef HV_EK
+    s.ekey = max(sm, (int)(um & 0x7fffffffu));
+#else
     int e = 0;
 #define HV_EK(v) e = max(e, max(abskey(v.x), max(abskey(v.y), abskey(v.z))))
     HV_EK(v12); HV_EK(v43); HV_EK(v56); HV_EK(v87);
@@ -73,6 +86,7 @@ __device__ __forceinline__ void samples20(const double* X, Samples& s) {
     HV_EK(v15); HV_EK(v26); HV_EK(v48); HV_EK(v37);
 #undef HV_EK
     s.ekey = e;
+#endif
     // corners: det(d_xi x, d_eta x, d_zeta x) with the 3 edges at the corner
     s.c[0] = det3(v12, v14, v15);
     s.c[1] = det3(v12, v23, v26);

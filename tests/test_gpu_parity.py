@@ -377,3 +377,51 @@ def test_subdivision_node_count_equals_oracle_for_valid_hexes():
     st = stats.read()
     assert st["n_subdivided"] == sel.size
     assert st["n_nodes"] == int(ref["nodes"].sum())
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: corner scaled Jacobian and Ushakova Test 1
+# --------------------------------------------------------------------------
+
+def _quality_parity(coords, sj, t1):
+    ref = oracle.corner_quality_soa(coords)
+    nan_ref = np.isnan(ref["sj_min"])
+    assert np.array_equal(np.isnan(sj), nan_ref)
+    ok = ~nan_ref
+    assert np.max(np.abs(sj[ok] - ref["sj_min"][ok]), initial=0.0) <= 1e-13
+    sure = ref["near"] == 0
+    assert np.array_equal(t1[sure], ref["test1"][sure])
+    return ref
+
+
+@pytest.mark.parametrize("n", [1, 255, 257, 20011])
+def test_corner_quality_parity(n, golden_hexes):
+    coords = hexgen.ragged_soa(n, seed=300 + n, amp=0.45)
+    dev = torch.from_numpy(coords).cuda()
+    sj, t1 = hv.corner_quality_soa(dev)
+    torch.cuda.synchronize()
+    _quality_parity(coords, sj.cpu().numpy(), t1.cpu().numpy())
+
+
+def test_corner_quality_special_cases(golden_hexes):
+    U = pins.KAPPA.astype(float)
+    S = U.copy(); S[:, 0] += 0.5 * S[:, 1]
+    D = U.copy(); D[1] = D[0]                                   # zero-length corner edge
+    N = U.copy(); N[4, 2] = np.nan
+    X = np.stack([U, S, U * [-1, 1, 1], D, N, golden_hexes["fig7_invalid"][0], golden_hexes["fig5_invalid"][0]])
+    coords = hexgen.nodes_to_soa(X)
+    sj, t1 = hv.corner_quality_soa(torch.from_numpy(coords).cuda())
+    torch.cuda.synchronize()
+    sj, t1 = sj.cpu().numpy(), t1.cpu().numpy()
+    assert sj[0] == 1.0 and abs(sj[1] - 1 / np.sqrt(1.25)) <= 1e-15 and sj[2] == -1.0
+    assert np.isnan(sj[3]) and np.isnan(sj[4])
+    assert abs(sj[5] - 0.6471) < 5e-5                           # Fig. 7 caption "0.64"
+    assert t1.tolist() == [1, 1, 0, 0, 0, 1, 1]                  # Fig. 5 passes Test 1 (necessary only)
+    _quality_parity(coords, sj, t1)
+
+
+def test_corner_quality_indexed_config3_slice():
+    verts, idx = hexgen.indexed_config(3, start=777, count=50_000)
+    sj, t1 = hv.corner_quality_indexed(torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda())
+    torch.cuda.synchronize()
+    _quality_parity(hexgen.indexed_to_soa(verts, idx), sj.cpu().numpy(), t1.cpu().numpy())

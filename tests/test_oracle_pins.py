@@ -400,3 +400,52 @@ def test_config0_has_no_near_boundary_hexes():
     assert o["near"].sum() == 0
     f = o["flags"]
     assert np.all((f & 3) != oracle.UNDETERMINED)
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: corner screening quantities
+# --------------------------------------------------------------------------
+
+def test_corner_quality_closed_forms():
+    """Unit cube: scaled Jacobian 1; shear x += s*y: every corner frame has det 1 and one
+    edge of length sqrt(1+s^2), so the min is 1/sqrt(1+s^2); mirrored cube: -1, Test 1 fails."""
+    assert oracle.corner_quality(U) == {"sj_min": 1.0, "test1": 1, "near": 0}
+    for s in (0.25, 0.5, 2.0):
+        X = U.copy()
+        X[:, 0] += s * X[:, 1]
+        r = oracle.corner_quality(X)
+        assert abs(r["sj_min"] - 1.0 / np.sqrt(1.0 + s * s)) <= 1e-15 and r["test1"] == 1
+    M = U * np.array([-1.0, 1.0, 1.0])
+    r = oracle.corner_quality(M)
+    assert r["sj_min"] == -1.0 and r["test1"] == 0
+
+
+def test_corner_quality_fig7_and_fig5(golden_hexes):
+    """Fig. 7 caption: corner scaled Jacobian "0.64" (0.6471 truncated, reading G10);
+    Fig. 5: all corner tets positive (Test 1 passes) although the hex is invalid."""
+    r7 = oracle.corner_quality(golden_hexes["fig7_invalid"][0])
+    assert abs(r7["sj_min"] - 0.64) < 0.01 and abs(r7["sj_min"] - 0.6471) < 5e-5
+    r5 = oracle.corner_quality(golden_hexes["fig5_invalid"][0])
+    assert r5["test1"] == 1
+    assert (oracle.check_hex(golden_hexes["fig5_invalid"][0])["flags"] & 3) == oracle.INVALID
+
+
+def test_corner_quality_invariances_and_test1_definition():
+    """Invariant under rotation, translation and positive scaling; Test 1 == all corner
+    samples > 0 (independent exact rational evaluation); Test 1 is necessary for validity."""
+    rng = np.random.default_rng(21)
+    for X in pins.random_hexes(200, 0.45, 22):
+        r = oracle.corner_quality(X)
+        Q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        if np.linalg.det(Q) < 0:
+            Q[:, 0] *= -1
+        Y = (X @ Q.T) * 3.7 + rng.normal(size=3)
+        r2 = oracle.corner_quality(Y)
+        assert abs(r["sj_min"] - r2["sj_min"]) <= 1e-12
+        exact_pos = all(pins.detj_exact(X, k) > 0 for k in range(8))
+        assert r["test1"] == int(exact_pos)
+        if (oracle.check_hex(X)["flags"] & 3) == oracle.VALID:
+            assert r["test1"] == 1
+    X = U.copy()
+    X[1] = X[0]                                  # zero-length corner edge: undefined metric
+    assert np.isnan(oracle.corner_quality(X)["sj_min"])
