@@ -67,8 +67,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
-    p.add_argument("--op", choices=["check", "quality"], default="check",
-                   help="check: the hot path (headline); quality: NEXT-2 corner screening kernel")
+    p.add_argument("--op", choices=["check", "quality", "bounds"], default="check",
+                   help="check: the hot path (headline); quality: NEXT-2 corner screening kernel; "
+                        "bounds: NEXT-1 certified min det J bounds")
+    p.add_argument("--rel-tol", type=float, default=1e-3, help="NEXT-1 tolerance (relative to max|b|)")
     p.add_argument("--variant", choices=["ldg", "wtma", "cp"], default=None,
                    help="pass-1 kernel variant for SoA inputs (sets HEXVAL_PASS1; default: the library's)")
     args = p.parse_args()
@@ -430,6 +432,25 @@ def run_op(args, world, rank, local):
                 hv.corner_quality_indexed(dev[0], dev[1], sj, t1)
         out_bytes = 9
         metric = "hexahedra screened/sec (corner scaled Jacobian + Test 1, fp64, 1 B200)"
+    elif args.op == "bounds":
+        lo = torch.empty(n, dtype=torch.float64, device="cuda")
+        up = torch.empty(n, dtype=torch.float64, device="cuda")
+        stt = torch.empty(n, dtype=torch.uint8, device="cuda")
+        nodes = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+        def step(count=None):
+            if layout == "soa":
+                hv.min_detj_bounds_soa(dev[0], args.rel_tol, lo, up, stt, nodes=count)
+            else:
+                hv.min_detj_bounds_indexed(dev[0], dev[1], args.rel_tol, lo, up, stt, nodes=count)
+        step(nodes)
+        torch.cuda.synchronize()
+        extra = {"rel_tol": args.rel_tol, "nodes_per_step": int(nodes.item()),
+                 "capped": int((stt & 1).sum().item())}
+        out_bytes = 17
+        metric = f"hexahedra bounded/sec (min det J to rel_tol {args.rel_tol:g}, fp64, 1 B200)"
+    if args.op != "bounds":
+        extra = {}
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
@@ -454,7 +475,7 @@ def run_op(args, world, rank, local):
             "config": {"workload": CONFIG_DESC[cfg], "layout": layout, "n_hexes_per_rank": n},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": algo},
-            "gpu_launches": args.steps, "clocks": clk.summary()}), flush=True)
+            "gpu_launches": args.steps, "clocks": clk.summary(), **extra}), flush=True)
     return 0
 
 

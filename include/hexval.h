@@ -138,6 +138,26 @@ int hexval_corner_quality_indexed(const double* vertices, const int32_t* hex_idx
                                   double* sj_min_out_opt, uint8_t* test1_out_opt,
                                   cudaStream_t stream);
 
+/* ---- NEXT-1: certified bounds on min det J ------------------------------------
+ * For every hex: lower_out[i] <= min over [0,1]^3 of det J <= upper_out[i] (device
+ * memory, n doubles each).  lower = min of the Bezier coefficients over the leaves of
+ * a subdivision tree (convex hull property), upper = min of the
+ * corner coefficients met (actual values); the bounds are
+ * "sharpened ... by subdividing": a subdomain is split while the
+ * min of its coefficients is < upper - tol, tol = rel_tol * max|b_root| (DESIGN.md
+ * reading G15), depth cap HEXVAL_MAX_DEPTH.  On return upper - lower <= tol unless
+ * status bit 0 (depth cap reached) is set.  status_out_opt (n bytes, may be NULL):
+ * bit 0 capped, bit 1 NONFINITE (then both bounds are NaN).  nodes_dev_opt: NULL or a
+ * device counter to which the number of split subdomains is added.
+ * rel_tol >= 0 (else HEXVAL_ERR_ARGUMENT).  Asynchronous on `stream`.           */
+int hexval_min_detj_bounds_soa(const double* coords, int64_t n, double rel_tol,
+                               double* lower_out, double* upper_out, uint8_t* status_out_opt,
+                               unsigned long long* nodes_dev_opt, cudaStream_t stream);
+int hexval_min_detj_bounds_indexed(const double* vertices, const int32_t* hex_idx, int64_t n,
+                                   double rel_tol, double* lower_out, double* upper_out,
+                                   uint8_t* status_out_opt, unsigned long long* nodes_dev_opt,
+                                   cudaStream_t stream);
+
 /* ---- host-resident calls (synchronous, end to end) --------------------------
  * Same layouts, but every pointer is HOST memory (pinned memory gives
  * overlapped copies; pageable memory works but serialises).  The library

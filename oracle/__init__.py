@@ -64,6 +64,11 @@ class OracleResult(ctypes.Structure):
         }
 
 
+class OracleBounds(ctypes.Structure):
+    _fields_ = [("lower", ctypes.c_double), ("upper", ctypes.c_double), ("tol", ctypes.c_double),
+                ("capped", ctypes.c_int), ("nodes", ctypes.c_int64)]
+
+
 _lib = None
 _D = ctypes.POINTER(ctypes.c_double)
 
@@ -100,6 +105,11 @@ def lib():
         L.oracle_corner_quality_soa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                                 ctypes.c_void_p, ctypes.c_int]
         L.oracle_corner_quality_soa.restype = None
+        L.oracle_min_detj_bounds.argtypes = [_D, ctypes.c_double, ctypes.POINTER(OracleBounds)]
+        L.oracle_min_detj_bounds.restype = None
+        L.oracle_min_detj_bounds_soa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p,
+                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        L.oracle_min_detj_bounds_soa.restype = None
         L.oracle_num_threads.argtypes = [ctypes.c_int]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
@@ -239,3 +249,20 @@ def corner_quality_soa(coords: np.ndarray, nthreads: int = 0) -> dict:
     lib().oracle_corner_quality_soa(coords.ctypes.data, n, sj.ctypes.data, t1.ctypes.data, nr.ctypes.data,
                                     int(nthreads))
     return {"sj_min": sj, "test1": t1, "near": nr}
+
+
+def min_detj_bounds(X, rel_tol: float) -> dict:
+    """NEXT-1: certified [lower, upper] on min det J with upper - lower <= rel_tol * max|b| (or capped)."""
+    X = _hex(X)
+    r = OracleBounds()
+    lib().oracle_min_detj_bounds(_dptr(X), float(rel_tol), ctypes.byref(r))
+    return {"lower": r.lower, "upper": r.upper, "tol": r.tol, "capped": r.capped, "nodes": r.nodes}
+
+
+def min_detj_bounds_soa(coords: np.ndarray, rel_tol: float, nthreads: int = 0) -> dict:
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    n = coords.shape[1]
+    lo, up, cap = np.zeros(n), np.zeros(n), np.zeros(n, np.uint8)
+    lib().oracle_min_detj_bounds_soa(coords.ctypes.data, n, float(rel_tol), lo.ctypes.data, up.ctypes.data,
+                                     cap.ctypes.data, int(nthreads))
+    return {"lower": lo, "upper": up, "capped": cap}

@@ -728,3 +728,67 @@ void oracle_corner_quality_soa(const double* coords, int64_t n, double* sj_out, 
         if (near_out) near_out[i] = (uint8_t)nr;
     }
 }
+
+/* -------------------------------------------------------------------------
+ * NEXT-1: bounds on min det J (min b <= min det J <= min
+ * of the corner coefficients; "sharpened as much as desired by subdividing").
+ * ---------------------------------------------------------------------- */
+static void bounds_rec(const double node[27], int depth, double tol, double* upper, double* lower,
+                       int* capped, int64_t* nodes) {
+    double child[8][27];
+    (*nodes)++;
+    for (int o = 0; o < 8; ++o) {                 /* children, and their corner values */
+        oracle_subdivide(node, o, child[o]);
+        const double mc = min_range(child[o], 0, 8);
+        if (mc < *upper) *upper = mc;
+    }
+    for (int o = 0; o < 8; ++o) {
+        const double m = min_range(child[o], 0, 27);
+        if (m >= *upper - tol) {                  /* cannot hide a value below upper - tol */
+            if (m < *lower) *lower = m;
+        } else if (depth + 1 >= ORACLE_MAX_DEPTH) {
+            if (m < *lower) *lower = m;
+            *capped = 1;
+        } else {
+            bounds_rec(child[o], depth + 1, tol, upper, lower, capped, nodes);
+        }
+    }
+}
+
+void oracle_min_detj_bounds(const double X[8][3], double rel_tol, oracle_bounds* r) {
+    memset(r, 0, sizeof(*r));
+    for (int k = 0; k < 8; ++k)
+        for (int a = 0; a < 3; ++a)
+            if (!coord_ok(X[k][a])) {
+                r->lower = r->upper = r->tol = NAN;
+                return;
+            }
+    double c[27], b[27];
+    oracle_samples27(X, c);
+    oracle_bezier_from_samples(c, b);
+    double scale = 0.0;
+    for (int s = 0; s < 27; ++s) scale = fmax(scale, fabs(b[s]));
+    r->tol = rel_tol * scale;
+    r->upper = min_range(b, 0, 8);
+    r->lower = INFINITY;
+    const double m = min_range(b, 0, 27);
+    if (m >= r->upper - r->tol) r->lower = m;
+    else bounds_rec(b, 0, r->tol, &r->upper, &r->lower, &r->capped, &r->nodes);
+}
+
+void oracle_min_detj_bounds_soa(const double* coords, int64_t n, double rel_tol, double* lower_out,
+                                double* upper_out, uint8_t* capped_out, int nthreads) {
+    const int nt = oracle_num_threads(nthreads);
+    (void)nt;
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nt)
+    for (int64_t i = 0; i < n; ++i) {
+        double X[8][3];
+        for (int k = 0; k < 8; ++k)
+            for (int a = 0; a < 3; ++a) X[k][a] = coords[(int64_t)(3 * k + a) * n + i];
+        oracle_bounds r;
+        oracle_min_detj_bounds(X, rel_tol, &r);
+        if (lower_out) lower_out[i] = r.lower;
+        if (upper_out) upper_out[i] = r.upper;
+        if (capped_out) capped_out[i] = (uint8_t)r.capped;
+    }
+}

@@ -80,6 +80,22 @@ int    oracle_classify_coeffs(const double b[27], double E, oracle_result* r);
  *   near    1 iff some corner det J is within its fp64 rounding bound of 0.
  * A NONFINITE hex (reading G13) gives sj_min = NaN, test1 = 0. */
 void   oracle_corner_quality(const double X[8][3], double* sj_min, int* test1, int* near);
+
+/* NEXT-1, bounds on min det J (reading G15 in DESIGN.md):
+ *   lower = min of the Bezier coefficients of the leaves of a subdivision tree (convex
+ *           hull property), upper = min of all corner coefficients met (actual values);
+ *   depth-first recursion in Fig. 3 child order; a node is split iff the min of its
+ *   coefficients is < upper - tol, tol = rel_tol * max|b_root|; depth cap 20 (a leaf
+ *   at the cap sets `capped`).  Without the cap, upper - lower <= tol on return.
+ *   NONFINITE input gives NaN bounds. */
+typedef struct oracle_bounds {
+    double lower, upper, tol;
+    int capped;
+    int64_t nodes;          /* nodes split */
+} oracle_bounds;
+void   oracle_min_detj_bounds(const double X[8][3], double rel_tol, oracle_bounds* r);
+void   oracle_min_detj_bounds_soa(const double* coords, int64_t n, double rel_tol, double* lower_out,
+                                  double* upper_out, uint8_t* capped_out, int nthreads);
 void   oracle_corner_quality_soa(const double* coords, int64_t n, double* sj_out, uint8_t* test1_out,
                                  uint8_t* near_out, int nthreads);
 

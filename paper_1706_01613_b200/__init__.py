@@ -23,7 +23,8 @@ __all__ = [
     "INVALID", "VALID", "UNDETERMINED", "NONFINITE", "FLAG_SUBDIVIDED", "MAX_DEPTH",
     "HexvalError", "lib", "library_path", "check_soa", "check_indexed", "check_soa_host",
     "check_indexed_host", "classify_bezier", "Stats", "Profile", "status_string", "version",
-    "kernel_launches_per_call", "corner_quality_soa", "corner_quality_indexed",
+    "kernel_launches_per_call", "corner_quality_soa", "corner_quality_indexed", "min_detj_bounds_soa",
+    "min_detj_bounds_indexed",
 ]
 
 INVALID, VALID, UNDETERMINED, NONFINITE = 0, 1, 2, 3
@@ -69,6 +70,10 @@ def _load() -> ctypes.CDLL:
     L.hexval_corner_quality_indexed.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp]
     L.hexval_corner_quality_soa.restype = ctypes.c_int
     L.hexval_corner_quality_indexed.restype = ctypes.c_int
+    L.hexval_min_detj_bounds_soa.argtypes = [_vp, _i64, ctypes.c_double, _vp, _vp, _vp, _vp, _vp]
+    L.hexval_min_detj_bounds_indexed.argtypes = [_vp, _vp, _i64, ctypes.c_double, _vp, _vp, _vp, _vp, _vp]
+    L.hexval_min_detj_bounds_soa.restype = ctypes.c_int
+    L.hexval_min_detj_bounds_indexed.restype = ctypes.c_int
     L.hexval_status_string.argtypes = [ctypes.c_int]
     L.hexval_status_string.restype = ctypes.c_char_p
     L.hexval_profile_create.argtypes = []
@@ -334,3 +339,44 @@ def corner_quality_indexed(vertices, hex_idx, sj_min=None, test1=None, stream=No
                                                test1.data_ptr(), _stream_handle(stream)),
            "hexval_corner_quality_indexed")
     return sj_min, test1
+
+
+def _bounds_outputs(n, device, lower, upper, status):
+    torch = _torch()
+    lower = torch.empty(n, dtype=torch.float64, device=device) if lower is None else lower
+    upper = torch.empty(n, dtype=torch.float64, device=device) if upper is None else upper
+    status = torch.empty(n, dtype=torch.uint8, device=device) if status is None else status
+    _require(lower, torch.float64, "lower")
+    _require(upper, torch.float64, "upper")
+    _require(status, torch.uint8, "status")
+    return lower, upper, status
+
+
+def min_detj_bounds_soa(coords, rel_tol: float, lower=None, upper=None, status=None, nodes=None, stream=None):
+    """hexval_min_detj_bounds_soa (NEXT-1): certified [lower, upper] on min det J per hex.
+
+    ``nodes``: optional int64 CUDA tensor of one element to which the split count is added."""
+    torch = _torch()
+    _require(coords, torch.float64, "coords", 2)
+    if coords.shape[0] != 24:
+        raise ValueError("coords must have shape (24, n)")
+    n = coords.shape[1]
+    lower, upper, status = _bounds_outputs(n, coords.device, lower, upper, status)
+    _check(lib().hexval_min_detj_bounds_soa(coords.data_ptr(), n, float(rel_tol), lower.data_ptr(), upper.data_ptr(),
+                                            status.data_ptr(), nodes.data_ptr() if nodes is not None else None,
+                                            _stream_handle(stream)), "hexval_min_detj_bounds_soa")
+    return lower, upper, status
+
+
+def min_detj_bounds_indexed(vertices, hex_idx, rel_tol: float, lower=None, upper=None, status=None, nodes=None,
+                            stream=None):
+    torch = _torch()
+    _require(vertices, torch.float64, "vertices", 2)
+    _require(hex_idx, torch.int32, "hex_idx", 2)
+    n = hex_idx.shape[0]
+    lower, upper, status = _bounds_outputs(n, hex_idx.device, lower, upper, status)
+    _check(lib().hexval_min_detj_bounds_indexed(vertices.data_ptr(), hex_idx.data_ptr(), n, float(rel_tol),
+                                                lower.data_ptr(), upper.data_ptr(), status.data_ptr(),
+                                                nodes.data_ptr() if nodes is not None else None,
+                                                _stream_handle(stream)), "hexval_min_detj_bounds_indexed")
+    return lower, upper, status

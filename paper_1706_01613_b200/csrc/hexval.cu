@@ -151,7 +151,9 @@ __device__ __forceinline__ int step2_class(const Samples& s, double tau2) {
 #pragma unroll
     for (int e = 0; e < 12; ++e) km = min(km, key(s.d[e]));
     if (km > T) return ST_VALID;                       // every sample > tau2 > 0: robustly positive
-#ifdef HEXVAL_STEP2_FP
+#ifndef HEXVAL_STEP2_INT
+    // slow path with FP64 compares (measured faster on config 1 than the
+    // integer-pipe variant below: 337 vs 349 us, 3 interleaved A/B runs)
     bool neg = false, amb = false;
 #pragma unroll
     for (int k = 0; k < 8; ++k) { neg |= s.c[k] < -tau2; amb |= fabs(s.c[k]) <= tau2; }
@@ -670,6 +672,46 @@ __device__ __forceinline__ void line_split(double p0, double p1, double p2, doub
     m = __fma_rn(0.25, p0, __fma_rn(0.25, p2, h1));
 }
 
+// xi split of a node P (layout i + 3j + 9k) into G1[a + 5j + 15k], a = 0..4
+// (both halves: the left child takes a = 0..2, the right one a = 2..4).
+__device__ __forceinline__ void split_xi(const double* P, double* G1) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const double p0 = P[3 * j + 9 * k], p1 = P[1 + 3 * j + 9 * k], p2 = P[2 + 3 * j + 9 * k];
+            double m01, m, m12;
+            line_split(p0, p1, p2, m01, m, m12);
+            double* g = G1 + 5 * j + 15 * k;
+            g[0] = p0; g[1] = m01; g[2] = m; g[3] = m12; g[4] = p2;
+        }
+}
+
+// Quarter (hx, hy) of the children: eta half hy of xi half hx of G1, then
+// both zeta halves: Z[a + 3u + 9v], xi index a (0..2), eta index u (0..2),
+// zeta index v (0..4); child hz takes v = 2hz .. 2hz+2.
+__device__ __forceinline__ void split_quarter(const double* G1, int hx, int hy, double* Z) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double B[9];                                     // B[u + 3k]: eta half hy of column a
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double* g = G1 + 2 * hx + a + 15 * k;
+            double m01, m, m12;
+            line_split(g[0], g[5], g[10], m01, m, m12);
+            if (hy == 0) { B[3 * k] = g[0]; B[1 + 3 * k] = m01; B[2 + 3 * k] = m; }
+            else { B[3 * k] = m; B[1 + 3 * k] = m12; B[2 + 3 * k] = g[10]; }
+        }
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            double m01, m, m12;
+            line_split(B[u], B[u + 3], B[u + 6], m01, m, m12);
+            double* z = Z + a + 3 * u;
+            z[0] = B[u]; z[9] = m01; z[18] = m; z[27] = m12; z[36] = B[u + 6];
+        }
+    }
+}
+
 struct K4Warp {
     unsigned status[32];    // per batch slot: bit 0 INVALID found, bit 1 depth cap reached
     uint32_t hex[32];       // hex id of each batch slot
@@ -763,18 +805,8 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
         const unsigned actmask = __ballot_sync(0xffffffffu, act);
         if (STATS && actmask) { nodes += __popc(actmask); maxd = max(maxd, d + 1); }
         // ---- split every active node into its 8 children --------------------
-        // xi split of P: G1[a + 5j + 15k], a = 0..4
         double G1[45];
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const double p0 = P[3 * j + 9 * k], p1 = P[1 + 3 * j + 9 * k], p2 = P[2 + 3 * j + 9 * k];
-                double m01, m, m12;
-                line_split(p0, p1, p2, m01, m, m12);
-                double* g = G1 + 5 * j + 15 * k;
-                g[0] = p0; g[1] = m01; g[2] = m; g[3] = m12; g[4] = p2;
-            }
+        split_xi(P, G1);
         bool inval = false, capped = false;
         int pushed = 0;                                  // warp-uniform
         const bool can_push = d + 1 < MAX_DEPTH;
@@ -782,27 +814,8 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
         for (int hx = 0; hx < 2; ++hx)
 #pragma unroll
             for (int hy = 0; hy < 2; ++hy) {
-                // Z[a + 3u + 9v]: xi index a (0..2), eta index u (0..2), zeta index v (0..4)
                 double Z[45];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    double B[9];                         // B[u + 3k]: eta half hy of column a
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        const double* g = G1 + 2 * hx + a + 15 * k;
-                        double m01, m, m12;
-                        line_split(g[0], g[5], g[10], m01, m, m12);
-                        if (hy == 0) { B[3 * k] = g[0]; B[1 + 3 * k] = m01; B[2 + 3 * k] = m; }
-                        else { B[3 * k] = m; B[1 + 3 * k] = m12; B[2 + 3 * k] = g[10]; }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 3; ++u) {
-                        double m01, m, m12;
-                        line_split(B[u], B[u + 3], B[u + 6], m01, m, m12);
-                        double* z = Z + a + 3 * u;
-                        z[0] = B[u]; z[9] = m01; z[18] = m; z[27] = m12; z[36] = B[u + 6];
-                    }
-                }
+                split_quarter(G1, hx, hy, Z);
                 // classify the two children (zeta halves hz = 0, 1)
                 bool push[2];
 #pragma unroll
@@ -878,6 +891,191 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-1: certified bounds on min det J: lower =
+// min of the Bezier coefficients over the leaves of a subdivision tree (convex
+// hull property), upper = min of every corner coefficient met (actual values
+// of det J).  A node is split iff min(b) < upper - tol, tol = rel_tol *
+// max|b_root| (reading G15), so on return upper - lower <= tol unless the
+// depth cap was reached.  Same warp-cooperative machinery as K4: every hex of
+// [0, n) is a batch entry; the per-hex upper/lower live in shared memory as
+// order-preserving 64-bit keys updated with atomicMin.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long okey(double x) {     // unsigned order == double order
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double okey_inv(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+
+struct BWarp {
+    unsigned long long upper[32], lower[32];
+    double tol[32];
+    unsigned capped[32];
+    uint32_t hex[32];
+    int cnt[MAX_DEPTH + 1];
+};
+
+template <class L>
+__global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, int64_t n, double rel_tol, double* __restrict__ lower_out,
+                                                            double* __restrict__ upper_out, uint8_t* __restrict__ status_out,
+                                                            unsigned* next, WarpStacks ws, unsigned long long* nodes_out) {
+    __shared__ BWarp wst[K4_WARPS];
+    const int lane = threadIdx.x & 31;
+    BWarp& W = wst[threadIdx.x >> 5];
+    const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
+    double* const sc = ws.coef + gw * 27 * K4_CAP;
+    unsigned char* const so = ws.owner + gw * K4_CAP;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    if (lane <= MAX_DEPTH) W.cnt[lane] = 0;
+    __syncwarp();
+    int top = 0, D = 0, nb = 0;
+    unsigned long long nodes = 0;
+    for (;;) {
+        double P[27];
+        bool act = false;
+        int owner = lane, d;
+        if (top == 0) {
+            if (lane < nb) {                              // batch done
+                const uint32_t h = W.hex[lane];
+                const bool nf = W.capped[lane] & 2u;
+                lower_out[h] = nf ? __longlong_as_double(0x7ff8000000000000ll) : okey_inv(W.lower[lane]);
+                upper_out[h] = nf ? __longlong_as_double(0x7ff8000000000000ll) : okey_inv(W.upper[lane]);
+                if (status_out) status_out[h] = (uint8_t)W.capped[lane];
+            }
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(next, 32u);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            nb = base < n ? (int)min((int64_t)32, n - (int64_t)base) : 0;
+            if (nb == 0) break;
+            d = 0;
+            if (lane < nb) {
+                const uint32_t h = base + lane;
+                W.hex[lane] = h;
+                W.capped[lane] = 0;
+                double X[24];
+                ld.load(h, X);
+                if (out_of_range(X)) {
+                    W.capped[lane] = 2;                      // NONFINITE: NaN bounds
+                    W.upper[lane] = W.lower[lane] = 0;
+                    W.tol[lane] = 0;
+                } else {
+                    Samples smp;
+                    samples20(X, smp);
+                    Coeffs t;
+                    transform(smp, t);
+                    root_coeffs(smp, t, P);
+                    double up = P[0], mn = P[0], sc_ = fabs(P[0]);
+#pragma unroll
+                    for (int c = 1; c < 27; ++c) { mn = dmin(mn, P[c]); sc_ = fmax(sc_, fabs(P[c])); }
+                    up = dmin(dmin(dmin(P[0], P[2]), dmin(P[6], P[8])), dmin(dmin(P[18], P[20]), dmin(P[24], P[26])));
+                    const double tol = __dmul_rn(rel_tol, sc_);
+                    W.tol[lane] = tol;
+                    W.upper[lane] = okey(up);
+                    W.lower[lane] = okey(mn >= up - tol ? mn : __longlong_as_double(0x7ff0000000000000ll));
+                    act = !(mn >= up - tol);                  // split the root
+                }
+            }
+        } else {
+            const int k = min(32, W.cnt[D]);
+            d = D;
+            if (lane < k) {
+                const int slot = top - k + lane;
+#pragma unroll
+                for (int c = 0; c < 27; ++c) P[c] = sc[(size_t)c * K4_CAP + slot];
+                owner = so[slot];
+                // upper may have dropped since the push: the node may now be a leaf
+                double mn = P[0];
+#pragma unroll
+                for (int c = 1; c < 27; ++c) mn = dmin(mn, P[c]);
+                const double U = okey_inv(W.upper[owner]);
+                if (mn >= U - W.tol[owner]) atomicMin(&W.lower[owner], okey(mn));
+                else act = true;
+            }
+            top -= k;
+            __syncwarp();
+            if (lane == 0) W.cnt[D] -= k;
+        }
+        __syncwarp();
+        nodes += __popc(__ballot_sync(0xffffffffu, act));
+        double G1[45];
+        split_xi(P, G1);
+        int pushed = 0;
+        const bool can_push = d + 1 < MAX_DEPTH;
+        const double tol = W.tol[owner];
+#pragma unroll
+        for (int hx = 0; hx < 2; ++hx)
+#pragma unroll
+            for (int hy = 0; hy < 2; ++hy) {
+                double Z[45];
+                split_quarter(G1, hx, hy, Z);
+                double cmin[2], amin[2];
+#pragma unroll
+                for (int hz = 0; hz < 2; ++hz) {
+                    double mc = Z[9 * 2 * hz], ma = Z[9 * 2 * hz];
+#pragma unroll
+                    for (int v = 0; v < 3; ++v)
+#pragma unroll
+                        for (int u = 0; u < 3; ++u)
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {
+                                const double z = Z[a + 3 * u + 9 * (2 * hz + v)];
+                                ma = dmin(ma, z);
+                                if (a != 1 && u != 1 && v != 1) mc = dmin(mc, z);
+                            }
+                    cmin[hz] = mc;
+                    amin[hz] = ma;
+                }
+                if (act) atomicMin(&W.upper[owner], okey(dmin(cmin[0], cmin[1])));
+                __syncwarp();
+                const double U = okey_inv(W.upper[owner]);
+                bool push[2];
+#pragma unroll
+                for (int hz = 0; hz < 2; ++hz) {
+                    const bool leaf = act && (amin[hz] >= U - tol || !can_push);
+                    if (leaf) {
+                        atomicMin(&W.lower[owner], okey(amin[hz]));
+                        if (!(amin[hz] >= U - tol)) atomicOr(&W.capped[owner], 1u);   // depth cap
+                    }
+                    push[hz] = act && !leaf;
+                }
+                const unsigned b0 = __ballot_sync(0xffffffffu, push[0]);
+                const unsigned b1 = __ballot_sync(0xffffffffu, push[1]);
+                if (b0 | b1) {
+                    const int c0 = __popc(b0);
+#pragma unroll
+                    for (int hz = 0; hz < 2; ++hz) {
+                        const unsigned bm = hz ? b1 : b0;
+                        if (bm & (1u << lane)) {
+                            const int slot = top + pushed + (hz ? c0 : 0) + __popc(bm & lt_mask);
+#pragma unroll
+                            for (int v = 0; v < 3; ++v)
+#pragma unroll
+                                for (int u = 0; u < 3; ++u)
+#pragma unroll
+                                    for (int a = 0; a < 3; ++a)
+                                        sc[(size_t)(a + 3 * u + 9 * v) * K4_CAP + slot] = Z[a + 3 * u + 9 * (2 * hz + v)];
+                            so[slot] = (unsigned char)owner;
+                        }
+                    }
+                    pushed += c0 + __popc(b1);
+                }
+            }
+        top += pushed;
+        __syncwarp();
+        if (pushed) {
+            if (lane == 0) W.cnt[d + 1] += pushed;
+            D = d + 1;
+        } else {
+            while (D > 0 && W.cnt[D] == 0) --D;
+        }
+        __syncwarp();
+    }
+    if (nodes_out && lane == 0 && nodes) atomicAdd(nodes_out, nodes);
 }
 
 // ---------------------------------------------------------------------------
@@ -1208,6 +1406,39 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     return HEXVAL_OK;
 }
 
+template <class L>
+int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* upper, uint8_t* status,
+               unsigned long long* nodes_dev_opt, cudaStream_t stream) {
+    if (n == 0) return HEXVAL_OK;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return HEXVAL_ERR_CUDA;
+    const DeviceInfo& info = device_info<SoaLoader>(dev);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bounds_kernel<L>, K4_THREADS, 0);
+    if (occ < 1) occ = 1;
+    const int64_t batches = (n + 31) / 32;
+    int64_t blocks = (int64_t)info.sms * occ;
+    const int64_t need = (batches + K4_WARPS - 1) / K4_WARPS;
+    if (need < blocks) blocks = need;
+    const size_t warps = (size_t)blocks * K4_WARPS;
+    const size_t sc_bytes = warps * 27 * K4_CAP * sizeof(double);
+    const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
+    char* base = nullptr;
+    if (cudaMallocAsync((void**)&base, 256 + sc_bytes + so_bytes, stream) != cudaSuccess) {
+        cudaGetLastError();
+        return HEXVAL_ERR_ALLOC;
+    }
+    unsigned* next = reinterpret_cast<unsigned*>(base);
+    WarpStacks ws;
+    ws.coef = reinterpret_cast<double*>(base + 256);
+    ws.owner = reinterpret_cast<unsigned char*>(base + 256 + sc_bytes);
+    cudaMemsetAsync(next, 0, 256, stream);
+    bounds_kernel<L><<<(unsigned)blocks, K4_THREADS, 0, stream>>>(ld, n, rel_tol, lower, upper, status, next, ws,
+                                                                    nodes_dev_opt);
+    cudaFreeAsync(base, stream);
+    return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1265,6 +1496,28 @@ int hexval_corner_quality_indexed(const double* vertices, const int32_t* hex_idx
     quality_kernel<IdxLoader><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(IdxLoader{vertices, hex_idx}, n,
                                                                                sj_min_out_opt, test1_out_opt);
     return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
+}
+
+int hexval_min_detj_bounds_soa(const double* coords, int64_t n, double rel_tol, double* lower_out,
+                               double* upper_out, uint8_t* status_out_opt, unsigned long long* nodes_dev_opt,
+                               cudaStream_t stream) {
+    if (n < 0 || n > INT32_MAX || !(rel_tol >= 0.0)) return HEXVAL_ERR_ARGUMENT;
+    if (n > 0 && (!coords || !lower_out || !upper_out)) return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(coords, 8) || misaligned(lower_out, 8) || misaligned(upper_out, 8) || misaligned(nodes_dev_opt, 8))
+        return HEXVAL_ERR_ALIGNMENT;
+    return run_bounds(SoaLoader{coords, n}, n, rel_tol, lower_out, upper_out, status_out_opt, nodes_dev_opt, stream);
+}
+
+int hexval_min_detj_bounds_indexed(const double* vertices, const int32_t* hex_idx, int64_t n, double rel_tol,
+                                   double* lower_out, double* upper_out, uint8_t* status_out_opt,
+                                   unsigned long long* nodes_dev_opt, cudaStream_t stream) {
+    if (n < 0 || n > INT32_MAX || !(rel_tol >= 0.0)) return HEXVAL_ERR_ARGUMENT;
+    if (n > 0 && (!vertices || !hex_idx || !lower_out || !upper_out)) return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(vertices, 8) || misaligned(hex_idx, 4) || misaligned(lower_out, 8) || misaligned(upper_out, 8) ||
+        misaligned(nodes_dev_opt, 8))
+        return HEXVAL_ERR_ALIGNMENT;
+    return run_bounds(IdxLoader{vertices, hex_idx}, n, rel_tol, lower_out, upper_out, status_out_opt, nodes_dev_opt,
+                      stream);
 }
 
 int hexval_check_soa(const double* coords, int64_t n, uint8_t* flags_out, double* coeffs_out_opt,

@@ -425,3 +425,63 @@ def test_corner_quality_indexed_config3_slice():
     sj, t1 = hv.corner_quality_indexed(torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda())
     torch.cuda.synchronize()
     _quality_parity(hexgen.indexed_to_soa(verts, idx), sj.cpu().numpy(), t1.cpu().numpy())
+
+
+# --------------------------------------------------------------------------
+# NEXT-1: certified bounds on min det J
+# --------------------------------------------------------------------------
+
+def _bounds_parity(coords, rel_tol, lo, up, st):
+    """Both sides return intervals of width <= tol containing min det J; the refinement
+    orders differ (GPU: warp-parallel by levels; oracle: depth first), so what is unique is
+    checked: each interval contains the other's witness range and both are tol-tight."""
+    ref = oracle.min_detj_bounds_soa(coords, rel_tol)
+    X = hexgen.soa_to_nodes(coords)
+    nf = np.isnan(ref["lower"])
+    assert np.array_equal(np.isnan(lo), nf) and np.array_equal(np.isnan(up), nf)
+    assert np.all((st[nf] & 2) == 2)
+    ok = ~nf
+    tol = np.array([rel_tol * np.abs(oracle.check_hex(X[j])["b"]).max() if ok[j] else 0 for j in range(len(lo))])
+    eps = 1e-12 * np.maximum(1.0, np.abs(up))
+    capped = ((st & 1) == 1) | (ref["capped"] == 1)
+    tight = ok & ~capped
+    assert np.all(up[tight] - lo[tight] <= tol[tight] + eps[tight])
+    # the true minimum lies in both intervals: they overlap, and each lower is below the other's upper
+    assert np.all(lo[ok] <= ref["upper"][ok] + eps[ok]) and np.all(ref["lower"][ok] <= up[ok] + eps[ok])
+    assert np.all(np.abs(up[tight] - ref["upper"][tight]) <= tol[tight] + eps[tight])
+    assert np.all(np.abs(lo[tight] - ref["lower"][tight]) <= tol[tight] + eps[tight])
+    return ref
+
+
+@pytest.mark.parametrize("rel_tol", [1e-2, 1e-5])
+def test_min_detj_bounds_random(rel_tol):
+    coords = hexgen.ragged_soa(5003, seed=41, amp=0.5)
+    lo, up, st = hv.min_detj_bounds_soa(torch.from_numpy(coords).cuda(), rel_tol)
+    torch.cuda.synchronize()
+    _bounds_parity(coords, rel_tol, lo.cpu().numpy(), up.cpu().numpy(), st.cpu().numpy())
+
+
+def test_min_detj_bounds_closed_forms(golden_hexes):
+    coords, r = hexgen.adversarial_config(3000, seed=4, start=9000)
+    U = pins.KAPPA.astype(float)
+    N = U.copy(); N[2, 1] = np.inf
+    extra = np.stack([U, U * [2, 3, 4], N, golden_hexes["fig5_invalid"][0], golden_hexes["fig6_valid"][0],
+                      golden_hexes["fig7_invalid"][0]])
+    coords = np.ascontiguousarray(np.concatenate([coords, hexgen.nodes_to_soa(extra)], axis=1))
+    rel_tol = 1e-4
+    nodes = torch.zeros(1, dtype=torch.int64, device="cuda")
+    lo, up, st = hv.min_detj_bounds_soa(torch.from_numpy(coords).cuda(), rel_tol, nodes=nodes)
+    torch.cuda.synchronize()
+    lo, up, st = lo.cpu().numpy(), up.cpu().numpy(), st.cpu().numpy()
+    _bounds_parity(coords, rel_tol, lo, up, st)
+    m = r.size
+    X = hexgen.soa_to_nodes(coords)
+    for j in range(m):                                         # min det J = r * volume (closed form)
+        b = oracle.check_hex(X[j])["b"]
+        m_star = r[j] * b.mean()
+        eps = 1e-12 * np.abs(b).max()
+        assert lo[j] <= m_star + eps <= up[j] + 2 * eps
+    assert lo[m] == up[m] == 1.0 and lo[m + 1] == up[m + 1] == 24.0
+    assert np.isnan(lo[m + 2]) and st[m + 2] == 2
+    assert up[m + 3] < 0 and lo[m + 4] > 0 and up[m + 5] < 0      # Figs. 5, 6, 7
+    assert int(nodes.item()) > 0

@@ -449,3 +449,62 @@ def test_corner_quality_invariances_and_test1_definition():
     X = U.copy()
     X[1] = X[0]                                  # zero-length corner edge: undefined metric
     assert np.isnan(oracle.corner_quality(X)["sj_min"])
+
+
+# --------------------------------------------------------------------------
+# NEXT-1: bounds on min det J
+# --------------------------------------------------------------------------
+
+def test_bounds_parallelepiped_and_cube():
+    """Affine map: det J constant, every coefficient equals det A, so lower = upper = det A."""
+    assert oracle.min_detj_bounds(U, 0.0) == {"lower": 1.0, "upper": 1.0, "tol": 0.0, "capped": 0, "nodes": 0}
+    rng = np.random.default_rng(31)
+    for _ in range(50):
+        A = rng.normal(size=(3, 3))
+        X = U @ A.T + rng.normal(size=3)
+        d = np.linalg.det(A)
+        r = oracle.min_detj_bounds(X, 1e-9)
+        assert abs(r["lower"] - d) <= 1e-12 * max(1, abs(d)) and abs(r["upper"] - d) <= 1e-12 * max(1, abs(d))
+
+
+@pytest.mark.parametrize("rel_tol,family", [(1e-2, "both"), (1e-4, "both"), (1e-9, "pushed")])
+def test_bounds_closed_form_families(rel_tol, family):
+    """Pushed-corner and twisted-prism families (DESIGN.md input recipe): min det J = r * V
+    in closed form, V = mean(b) = volume; the bounds must bracket it within tol.  (The
+    twisted prisms attain their minimum on a plane, so their tree grows like 1/tol.)"""
+    coords, r = hexgen.adversarial_config(120, seed=4, start=9000)
+    X = hexgen.soa_to_nodes(coords)
+    for j in range(X.shape[0]):
+        if family == "pushed" and j % 2:
+            continue
+        b = oracle.check_hex(X[j])["b"]
+        m_star = r[j] * b.mean()
+        res = oracle.min_detj_bounds(X[j], rel_tol)
+        eps = 1e-12 * np.abs(b).max()
+        assert res["lower"] <= m_star + eps and m_star <= res["upper"] + eps, (j, res, m_star)
+        assert res["capped"] or res["upper"] - res["lower"] <= res["tol"] + eps
+
+
+def test_bounds_paper_figures(golden_hexes):
+    """Figs. 5 and 7 are invalid (captions): upper < 0; Fig. 6 is valid: lower > 0."""
+    assert oracle.min_detj_bounds(golden_hexes["fig5_invalid"][0], 1e-6)["upper"] < 0
+    assert oracle.min_detj_bounds(golden_hexes["fig7_invalid"][0], 1e-6)["upper"] < 0
+    assert oracle.min_detj_bounds(golden_hexes["fig6_valid"][0], 1e-6)["lower"] > 0
+
+
+def test_bounds_against_dense_sampling_and_verdicts():
+    """Dense 31^3 sampling of det J (independent evaluation) never goes below lower, and
+    lies above upper - tol; lower > 0 implies VALID and upper <= 0 implies INVALID."""
+    P = pins.grid_points(30)
+    for X in pins.random_hexes(60, 0.5, 33):
+        res = oracle.min_detj_bounds(X, 1e-3)
+        v = pins.detj(X, P)
+        scale = max(1.0, np.abs(v).max())
+        assert v.min() >= res["lower"] - 1e-12 * scale
+        assert v.min() >= res["upper"] - res["tol"] - 1e-12 * scale
+        flags = oracle.check_hex(X)
+        if not flags["near_boundary"]:
+            if res["lower"] > 0:
+                assert (flags["flags"] & 3) == oracle.VALID
+            if res["upper"] <= 0:
+                assert (flags["flags"] & 3) == oracle.INVALID
