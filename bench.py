@@ -67,9 +67,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
-    p.add_argument("--op", choices=["check", "quality", "bounds"], default="check",
+    p.add_argument("--op", choices=["check", "quality", "bounds", "select", "quads"], default="check",
                    help="check: the hot path (headline); quality: NEXT-2 corner screening kernel; "
-                        "bounds: NEXT-1 certified min det J bounds")
+                        "bounds: NEXT-1 certified min det J bounds; select: NEXT-3 candidate filtering "
+                        "(on the config's flags); quads: NEXT-4 linear quadrangles (10M, noise 0.35)")
     p.add_argument("--rel-tol", type=float, default=1e-3, help="NEXT-1 tolerance (relative to max|b|)")
     p.add_argument("--variant", choices=["ldg", "wtma", "cp"], default=None,
                    help="pass-1 kernel variant for SoA inputs (sets HEXVAL_PASS1; default: the library's)")
@@ -418,10 +419,48 @@ def run_op(args, world, rank, local):
 
     torch.cuda.set_device(local)
     cfg = args.config
-    layout, n, host = make_inputs(cfg, rank)
+    if args.op == "quads":
+        import hexgen
+        from paper_1706_01613_b200 import shard
+        start, n = shard.weak_shard(10_000_000, rank)
+        layout, host = "quad-soa", (hexgen.quad_soa(n, 0.35, 5, start),)
+    else:
+        layout, n, host = make_inputs(cfg, rank)
     dev = [torch.from_numpy(a).cuda() for a in host]
     stream = torch.cuda.current_stream()
-    if args.op == "quality":
+    in_bytes = None
+    if args.op == "quads":
+        qf = torch.empty(n, dtype=torch.uint8, device="cuda")
+
+        def step():
+            hv.check_quad_soa(dev[0], qf)
+        out_bytes, in_bytes = 1, 64 * n
+        metric = "quadrangles validated/sec (fp64, 1 B200)"
+    elif args.op == "select":
+        flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+        if layout == "soa":
+            hv.check_soa(dev[0], flags=flags)
+        else:
+            hv.check_indexed(dev[0], dev[1], flags=flags)
+        groups = 99 ** 3 if cfg == 3 else 1000
+        grp = (torch.arange(n, device="cuda", dtype=torch.int64) % groups).to(torch.int32)
+        ids = torch.empty(n, dtype=torch.int32, device="cuda")
+        gcount = torch.zeros(groups, dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        lib = hv.lib()
+        handle = stream.cuda_stream
+
+        def step():                                   # the C ABI directly: no host read-back per step
+            lib.hexval_select_valid(flags.data_ptr(), n, grp.data_ptr(), groups, ids.data_ptr(), cnt.data_ptr(),
+                                    gcount.data_ptr(), handle)
+        step()
+        torch.cuda.synchronize()
+        n_valid = int(cnt.item())
+        in_bytes = 2 * n + 4 * n + 4 * n_valid        # flags read twice, group ids, scattered count updates
+        out_bytes = 0
+        extra_sel = {"n_valid": n_valid, "groups": groups}
+        metric = "candidates filtered/sec (VALID ids + per-cell counts, 1 B200)"
+    elif args.op == "quality":
         sj = torch.empty(n, dtype=torch.float64, device="cuda")
         t1 = torch.empty(n, dtype=torch.uint8, device="cuda")
 
@@ -450,7 +489,7 @@ def run_op(args, world, rank, local):
         out_bytes = 17
         metric = f"hexahedra bounded/sec (min det J to rel_tol {args.rel_tol:g}, fp64, 1 B200)"
     if args.op != "bounds":
-        extra = {}
+        extra = extra_sel if args.op == "select" else {}
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
@@ -465,14 +504,18 @@ def run_op(args, world, rank, local):
         torch.cuda.synchronize()
         barrier(world)
     ms = dist_max(ev0.elapsed_time(ev1) / args.steps, world)
-    algo = (192 * n if layout == "soa" else 32 * n + 24 * host[0].shape[0]) + out_bytes * n
+    if in_bytes is None:
+        in_bytes = 192 * n if layout == "soa" else 32 * n + 24 * host[0].shape[0]
+    algo = in_bytes + out_bytes * n + (4 * extra.get("n_valid", 0) if args.op == "select" else 0)
     peak, peak_src = measured_peaks()
     ach = algo / (ms * 1e-3) / 1e9
     if rank == 0:
         print(json.dumps({
             "op": args.op, "metric": metric, "value": world * n / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "ms_per_step": ms, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_DESC[cfg], "layout": layout, "n_hexes_per_rank": n},
+            "config": {"workload": ("10M linear quadrangles, unit square + U[-0.35,0.35]^2 noise, seed 5"
+                                    if args.op == "quads" else CONFIG_DESC[cfg]),
+                       "layout": layout, "n_per_rank": n},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": algo},
             "gpu_launches": args.steps, "clocks": clk.summary(), **extra}), flush=True)

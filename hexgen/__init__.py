@@ -33,7 +33,7 @@ import numpy as np
 __all__ = [
     "UNIT_CUBE", "splitmix64", "uniform", "soa_config", "indexed_config",
     "adversarial_config", "CONFIGS", "config_size", "make", "soa_to_nodes",
-    "nodes_to_soa", "indexed_to_soa", "ragged_soa",
+    "nodes_to_soa", "indexed_to_soa", "ragged_soa", "quad_soa", "UNIT_SQUARE",
 ]
 
 _G = np.uint64(0x9E3779B97F4A7C15)
@@ -339,6 +339,20 @@ def soa_to_nodes(coords: np.ndarray) -> np.ndarray:
 
 def indexed_to_soa(vertices: np.ndarray, hex_idx: np.ndarray) -> np.ndarray:
     return nodes_to_soa(vertices[hex_idx.astype(np.int64)])
+
+
+UNIT_SQUARE = np.array([[0, 0], [1, 0], [1, 1], [0, 1]], dtype=np.float64)
+
+
+def quad_soa(n: int, amp: float, seed: int, start: int = 0) -> np.ndarray:
+    """Linear quadrangles (NEXT-4): unit-square corner k + amp*(2r-1) per axis, r drawn at
+    (seed, stream=500+p, counter=i) for plane p = 2k + a.  Returns the (8, n) SoA block."""
+    idx = np.arange(start, start + n, dtype=np.uint64)
+    out = np.empty((8, n), dtype=np.float64)
+    for p in range(8):
+        k, a = divmod(p, 2)
+        out[p] = UNIT_SQUARE[k, a] + amp * (2.0 * uniform(seed, 500 + p, idx) - 1.0)
+    return out
 
 
 def ragged_soa(n: int, seed: int = 11, amp: float = 0.35) -> np.ndarray:

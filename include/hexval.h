@@ -158,6 +158,36 @@ int hexval_min_detj_bounds_indexed(const double* vertices, const int32_t* hex_id
                                    uint8_t* status_out_opt, unsigned long long* nodes_dev_opt,
                                    cudaStream_t stream);
 
+/* ---- NEXT-3: candidate-set filtering (indirect hex meshing) -------------------
+ * The paper's motivating workload checks candidate hexahedra built from a tet mesh
+ * and keeps the valid ones.  From a flags array (n
+ * bytes, as written by the calls above):
+ *   ids_out_opt       NULL or n int32: the ids i with (flags[i] & 3) == VALID in
+ *                     increasing order (the first *count_dev entries are written);
+ *   count_dev         device long long: number of VALID entries (required);
+ *   group_opt         NULL or n int32 group ids in [0, n_groups) (e.g. grid cell of
+ *                     candidate i); precondition, not checked;
+ *   group_counts_opt  NULL iff group_opt is NULL; n_groups int32 counters to which
+ *                     the number of VALID candidates of each group is ADDED (the
+ *                     caller zeroes them first).
+ * Device memory, asynchronous on `stream`.                                        */
+int hexval_select_valid(const uint8_t* flags, int64_t n, const int32_t* group_opt, int64_t n_groups,
+                        int32_t* ids_out_opt, long long* count_dev, int32_t* group_counts_opt,
+                        cudaStream_t stream);
+
+/* ---- NEXT-4: linear quadrangles (section 2.1) ---------
+ * coords      SoA, 8 planes of n doubles: coords[(2*k + a)*n + i] is axis a (x, y) of
+ *             node k = 0..3 of quad i, counter-clockwise (shape functions PAPER.md:290-297).
+ * flags_out   n bytes: VALID iff det J > 0 at all four corners (det J is bilinear, its
+ *             minimum is a corner value), INVALID otherwise (an exact
+ *             zero is INVALID, reading G2; values within the fp64 rounding bound of 0
+ *             are decided exactly), NONFINITE for a NaN/Inf or |x| > 2^300 coordinate.
+ * J_out_opt   NULL or 4*n doubles: J_out[k*n + i] = det J at corner k+1 (J1 = v12 x v14,
+ *             J2 = v12 x v23, J3 = v43 x v23, J4 = v43 x v14; reading Q1 in DESIGN.md).
+ * Device memory, asynchronous on `stream`.                                        */
+int hexval_check_quad_soa(const double* coords, int64_t n, uint8_t* flags_out, double* J_out_opt,
+                          cudaStream_t stream);
+
 /* ---- host-resident calls (synchronous, end to end) --------------------------
  * Same layouts, but every pointer is HOST memory (pinned memory gives
  * overlapped copies; pageable memory works but serialises).  The library

@@ -110,6 +110,13 @@ def lib():
         L.oracle_min_detj_bounds_soa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p,
                                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         L.oracle_min_detj_bounds_soa.restype = None
+        L.oracle_check_quad.argtypes = [_D, _D, ctypes.POINTER(ctypes.c_int)]
+        L.oracle_check_quad.restype = ctypes.c_int
+        L.oracle_exact_orient2d.argtypes = [_D, _D, _D]
+        L.oracle_exact_orient2d.restype = ctypes.c_int
+        L.oracle_check_quad_soa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_int]
+        L.oracle_check_quad_soa.restype = None
         L.oracle_num_threads.argtypes = [ctypes.c_int]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
@@ -266,3 +273,40 @@ def min_detj_bounds_soa(coords: np.ndarray, rel_tol: float, nthreads: int = 0) -
     lib().oracle_min_detj_bounds_soa(coords.ctypes.data, n, float(rel_tol), lo.ctypes.data, up.ctypes.data,
                                      cap.ctypes.data, int(nthreads))
     return {"lower": lo, "upper": up, "capped": cap}
+
+
+def select_valid(flags: np.ndarray, group: np.ndarray | None = None, n_groups: int = 0):
+    """NEXT-3: ids of the VALID candidates in increasing order,
+    and the number of VALID candidates per group.  Plain definition (numpy)."""
+    flags = np.asarray(flags, dtype=np.uint8)
+    valid = (flags & 3) == VALID
+    ids = np.flatnonzero(valid).astype(np.int32)
+    counts = None
+    if group is not None:
+        counts = np.bincount(np.asarray(group)[valid], minlength=n_groups).astype(np.int32)
+    return ids, counts
+
+
+def check_quad(Q) -> dict:
+    """NEXT-4: validity of a linear quadrangle (4x2 nodes, counter-clockwise)."""
+    Q = np.ascontiguousarray(np.asarray(Q, dtype=np.float64).reshape(4, 2))
+    J = np.zeros(4)
+    nr = ctypes.c_int()
+    f = lib().oracle_check_quad(_dptr(Q), _dptr(J), ctypes.byref(nr))
+    return {"flags": f, "J": J, "near": nr.value}
+
+
+def exact_orient2d(a, b, c) -> int:
+    a, b, c = (np.ascontiguousarray(np.asarray(v, dtype=np.float64)) for v in (a, b, c))
+    return lib().oracle_exact_orient2d(_dptr(a), _dptr(b), _dptr(c))
+
+
+def check_quad_soa(coords: np.ndarray, nthreads: int = 0) -> dict:
+    """Batch over a (8, n) SoA array: plane 2k + a = axis a of node k."""
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    n = coords.shape[1]
+    flags, near = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+    J = np.zeros((4, n))
+    lib().oracle_check_quad_soa(coords.ctypes.data, n, flags.ctypes.data, J.ctypes.data, near.ctypes.data,
+                                int(nthreads))
+    return {"flags": flags, "J": J, "near": near}

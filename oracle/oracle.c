@@ -792,3 +792,86 @@ void oracle_min_detj_bounds_soa(const double* coords, int64_t n, double rel_tol,
         if (capped_out) capped_out[i] = (uint8_t)r.capped;
     }
 }
+
+/* -------------------------------------------------------------------------
+ * NEXT-4: linear quadrangle, section 2.1 (lines 282-349): det J is
+ * bilinear, its minimum is at a corner, so the element is valid iff the four
+ * corner values are positive.
+ * ---------------------------------------------------------------------- */
+int oracle_exact_orient2d(const double a[2], const double b[2], const double c[2]) {
+    /* (b-a) x (c-a) = a x b + b x c + c x a with u x v = u_x v_y - u_y v_x: 6 products of
+     * input doubles, evaluated on integers after a common power-of-two scaling */
+    const double* P[3] = {a, b, c};
+    int64_t mant[3][2];
+    int expo[3][2], emin = INT32_MAX;
+    for (int k = 0; k < 3; ++k)
+        for (int t = 0; t < 2; ++t) {
+            int e = 0;
+            const double f = frexp(P[k][t], &e);
+            mant[k][t] = (int64_t)ldexp(f, 53);
+            expo[k][t] = e - 53;
+            if (mant[k][t] != 0 && expo[k][t] < emin) emin = expo[k][t];
+        }
+    if (emin == INT32_MAX) return 0;
+    big B[3][2];
+    for (int k = 0; k < 3; ++k)
+        for (int t = 0; t < 2; ++t) big_set_shifted(&B[k][t], mant[k][t], expo[k][t] - emin);
+    big acc;
+    memset(&acc, 0, sizeof(acc));
+    for (int k = 0; k < 3; ++k) {                 /* P_k x P_{k+1} */
+        const int l = (k + 1) % 3;
+        big t1, t2;
+        big_mul(&B[k][0], &B[l][1], &t1);
+        big_mul(&B[k][1], &B[l][0], &t2);
+        big_add(&acc, &t1, &acc);
+        big_sub(&acc, &t2, &acc);
+    }
+    return big_sign(&acc);
+}
+
+int oracle_check_quad(const double Q[4][2], double J[4], int* near) {
+    *near = 0;
+    for (int k = 0; k < 4; ++k)
+        for (int a = 0; a < 2; ++a)
+            if (!coord_ok(Q[k][a])) {
+                for (int q = 0; q < 4; ++q) J[q] = NAN;
+                return ORACLE_NONFINITE;
+            }
+    double v12[2], v43[2], v14[2], v23[2];
+    for (int a = 0; a < 2; ++a) {
+        v12[a] = Q[1][a] - Q[0][a];
+        v43[a] = Q[2][a] - Q[3][a];
+        v14[a] = Q[3][a] - Q[0][a];
+        v23[a] = Q[2][a] - Q[1][a];
+    }
+    const double* U[4] = {v12, v12, v43, v43};
+    const double* W[4] = {v14, v23, v23, v14};
+    /* corner k as an orientation (origin, xi-neighbour, eta-neighbour) of input points */
+    static const int ORI[4][3] = {{0, 1, 3}, {0, 1, 2}, {2, 3, 1}, {3, 0, 2}};
+    int valid = 1;
+    for (int k = 0; k < 4; ++k) {
+        J[k] = U[k][0] * W[k][1] - U[k][1] * W[k][0];
+        const double tau = 8.0 * U_ROUND * (fabs(U[k][0] * W[k][1]) + fabs(U[k][1] * W[k][0])) + ldexp(1.0, -1060);
+        if (fabs(J[k]) <= tau) *near = 1;
+        if (oracle_exact_orient2d(Q[ORI[k][0]], Q[ORI[k][1]], Q[ORI[k][2]]) <= 0) valid = 0;
+    }
+    return valid ? ORACLE_VALID : ORACLE_INVALID;
+}
+
+void oracle_check_quad_soa(const double* coords, int64_t n, uint8_t* flags_out, double* J_out,
+                           uint8_t* near_out, int nthreads) {
+    const int nt = oracle_num_threads(nthreads);
+    (void)nt;
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (int64_t i = 0; i < n; ++i) {
+        double Q[4][2], J[4];
+        int nr;
+        for (int k = 0; k < 4; ++k)
+            for (int a = 0; a < 2; ++a) Q[k][a] = coords[(int64_t)(2 * k + a) * n + i];
+        const int f = oracle_check_quad(Q, J, &nr);
+        if (flags_out) flags_out[i] = (uint8_t)f;
+        if (J_out)
+            for (int k = 0; k < 4; ++k) J_out[(int64_t)k * n + i] = J[k];
+        if (near_out) near_out[i] = (uint8_t)nr;
+    }
+}

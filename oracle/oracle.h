@@ -99,6 +99,17 @@ void   oracle_min_detj_bounds_soa(const double* coords, int64_t n, double rel_to
 void   oracle_corner_quality_soa(const double* coords, int64_t n, double* sj_out, uint8_t* test1_out,
                                  uint8_t* near_out, int nthreads);
 
+/* NEXT-4, linear quadrangle: Q[k][a], nodes 1..4 counter-clockwise
+ * (L1 = (1-xi)(1-eta), L2 = xi(1-eta), L3 = xi eta, L4 = (1-xi) eta).  J[k] = det J at
+ * corner k: J1 = v12 x v14, J2 = v12 x v23, J3 = v43 x v23, J4 = v43 x v14 (reading Q1).
+ * Returns the flags byte: VALID iff all four corner values are > 0, signs decided
+ * exactly; INVALID otherwise; NONFINITE for a non-finite or |x| > 2^300 coordinate.
+ * near = 1 iff some |J_k| is within its fp64 rounding bound of 0. */
+int    oracle_check_quad(const double Q[4][2], double J[4], int* near);
+int    oracle_exact_orient2d(const double a[2], const double b[2], const double c[2]); /* sign((b-a) x (c-a)) */
+void   oracle_check_quad_soa(const double* coords, int64_t n, uint8_t* flags_out, double* J_out,
+                             uint8_t* near_out, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,7 +24,7 @@ __all__ = [
     "HexvalError", "lib", "library_path", "check_soa", "check_indexed", "check_soa_host",
     "check_indexed_host", "classify_bezier", "Stats", "Profile", "status_string", "version",
     "kernel_launches_per_call", "corner_quality_soa", "corner_quality_indexed", "min_detj_bounds_soa",
-    "min_detj_bounds_indexed",
+    "min_detj_bounds_indexed", "select_valid", "check_quad_soa",
 ]
 
 INVALID, VALID, UNDETERMINED, NONFINITE = 0, 1, 2, 3
@@ -74,6 +74,10 @@ def _load() -> ctypes.CDLL:
     L.hexval_min_detj_bounds_indexed.argtypes = [_vp, _vp, _i64, ctypes.c_double, _vp, _vp, _vp, _vp, _vp]
     L.hexval_min_detj_bounds_soa.restype = ctypes.c_int
     L.hexval_min_detj_bounds_indexed.restype = ctypes.c_int
+    L.hexval_select_valid.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp]
+    L.hexval_select_valid.restype = ctypes.c_int
+    L.hexval_check_quad_soa.argtypes = [_vp, _i64, _vp, _vp, _vp]
+    L.hexval_check_quad_soa.restype = ctypes.c_int
     L.hexval_status_string.argtypes = [ctypes.c_int]
     L.hexval_status_string.restype = ctypes.c_char_p
     L.hexval_profile_create.argtypes = []
@@ -380,3 +384,50 @@ def min_detj_bounds_indexed(vertices, hex_idx, rel_tol: float, lower=None, upper
                                                 nodes.data_ptr() if nodes is not None else None,
                                                 _stream_handle(stream)), "hexval_min_detj_bounds_indexed")
     return lower, upper, status
+
+
+def select_valid(flags, group=None, n_groups: int = 0, ids=None, group_counts=None, stream=None):
+    """hexval_select_valid (NEXT-3): returns (ids[:count], count, group_counts).
+
+    ``count`` is read back to the host (one 8-byte D2H copy) to size the ids view."""
+    torch = _torch()
+    _require(flags, torch.uint8, "flags")
+    n = flags.numel()
+    if ids is None:
+        ids = torch.empty(n, dtype=torch.int32, device=flags.device)
+    _require(ids, torch.int32, "ids")
+    count = torch.zeros(1, dtype=torch.int64, device=flags.device)
+    if group is not None:
+        _require(group, torch.int32, "group")
+        if group_counts is None:
+            group_counts = torch.zeros(n_groups, dtype=torch.int32, device=flags.device)
+        _require(group_counts, torch.int32, "group_counts")
+    _check(lib().hexval_select_valid(flags.data_ptr(), n, group.data_ptr() if group is not None else None,
+                                     int(n_groups), ids.data_ptr(), count.data_ptr(),
+                                     group_counts.data_ptr() if group is not None else None,
+                                     _stream_handle(stream)), "hexval_select_valid")
+    c = int(count.item())
+    return ids[:c], c, group_counts
+
+
+def check_quad_soa(coords, flags=None, J=None, stream=None):
+    """hexval_check_quad_soa (NEXT-4): coords is an (8, n) float64 CUDA tensor (plane 2k + a).
+
+    Returns ``(flags, J)``; ``J`` is a (4, n) tensor of corner values when requested."""
+    torch = _torch()
+    _require(coords, torch.float64, "coords", 2)
+    if coords.shape[0] != 8:
+        raise ValueError("coords must have shape (8, n)")
+    n = coords.shape[1]
+    if flags is None:
+        flags = torch.empty(n, dtype=torch.uint8, device=coords.device)
+    _require(flags, torch.uint8, "flags")
+    if J is True:
+        J = torch.empty((4, n), dtype=torch.float64, device=coords.device)
+    elif J is False:
+        J = None
+    if J is not None:
+        _require(J, torch.float64, "J")
+    _check(lib().hexval_check_quad_soa(coords.data_ptr(), n, flags.data_ptr(), J.data_ptr() if J is not None else None,
+                                       _stream_handle(stream)), "hexval_check_quad_soa")
+    return flags, J

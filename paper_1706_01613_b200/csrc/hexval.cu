@@ -1079,6 +1079,185 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, int64_t n, dou
 }
 
 // ---------------------------------------------------------------------------
+// NEXT-3: candidate-set filtering for indirect hex meshing (PAPER.md:80-85,
+// 1247-1250): the ids of the VALID candidates in increasing order, and
+// optionally the number of VALID candidates per group (e.g. per grid cell).
+// Three kernels: per-tile counts (16 flags per thread, one 16-B load), a
+// one-CTA exclusive scan of the tile counts, and the ordered write.
+// ---------------------------------------------------------------------------
+constexpr int SEL_THREADS = 256;
+constexpr int SEL_TILE = SEL_THREADS * 16;
+
+__device__ __forceinline__ unsigned valid_mask16(const uint8_t* __restrict__ flags, int64_t n, int64_t i0) {
+    unsigned m = 0;
+    if (i0 + 16 <= n && ((((uintptr_t)(flags + i0)) & 15) == 0)) {
+        const uint4 w = __ldcs(reinterpret_cast<const uint4*>(flags + i0));
+        const unsigned ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) m |= ((((ws[q] >> (8 * b)) & 3u) == HEXVAL_VALID) ? 1u : 0u) << (4 * q + b);
+    } else {
+#pragma unroll
+        for (int b = 0; b < 16; ++b)
+            if (i0 + b < n && (flags[i0 + b] & 3) == HEXVAL_VALID) m |= 1u << b;
+    }
+    return m;
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) select_count_kernel(const uint8_t* __restrict__ flags, int64_t n,
+                                                                     const int32_t* __restrict__ group,
+                                                                     int32_t* __restrict__ group_counts,
+                                                                     unsigned* __restrict__ tile_counts) {
+    __shared__ unsigned s_w[SEL_THREADS / 32];
+    const int64_t i0 = (int64_t)blockIdx.x * SEL_TILE + (int64_t)threadIdx.x * 16;
+    const unsigned m = valid_mask16(flags, n, i0);
+    if (group_counts && m) {
+#pragma unroll 1
+        for (unsigned r = m; r; r &= r - 1) atomicAdd(&group_counts[__ldg(group + i0 + __ffs(r) - 1)], 1);
+    }
+    unsigned c = __popc(m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = 0;
+#pragma unroll
+        for (int w = 0; w < SEL_THREADS / 32; ++w) t += s_w[w];
+        tile_counts[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of `tiles` counts in place (one CTA), total to *count
+__global__ void __launch_bounds__(1024) select_scan_kernel(unsigned* __restrict__ tile_counts, int64_t tiles,
+                                                             long long* __restrict__ count) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t base = 0; base < tiles; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        const unsigned long long v = i < tiles ? tile_counts[i] : 0;
+        unsigned long long x = v;                                   // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            unsigned long long z = s_w[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, z, o);
+                if (lane >= o) z += y;
+            }
+            s_w[lane] = z;                                           // inclusive over warps
+        }
+        __syncthreads();
+        const unsigned long long excl = s_carry + (w ? s_w[w - 1] : 0) + x - v;
+        if (i < tiles) tile_counts[i] = (unsigned)excl;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += s_w[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count = (long long)s_carry;
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) select_write_kernel(const uint8_t* __restrict__ flags, int64_t n,
+                                                                     const unsigned* __restrict__ tile_offsets,
+                                                                     int32_t* __restrict__ ids) {
+    __shared__ unsigned s_w[SEL_THREADS / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * SEL_TILE + (int64_t)threadIdx.x * 16;
+    const unsigned m = valid_mask16(flags, n, i0);
+    const unsigned c = __popc(m);
+    unsigned x = c;                                                  // inclusive warp scan of counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    unsigned before = 0;
+#pragma unroll
+    for (int q = 0; q < SEL_THREADS / 32; ++q) before += q < w ? s_w[q] : 0u;
+    unsigned pos = tile_offsets[blockIdx.x] + before + x - c;
+#pragma unroll 1
+    for (unsigned r = m; r; r &= r - 1) ids[pos++] = (int32_t)(i0 + __ffs(r) - 1);
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-4: linear quadrangle (section 2.1).  det J is
+// bilinear, its minimum is at a corner: VALID iff J1..J4 > 0.  One quad per
+// thread, 8 coordinate planes (plane 2k+a); a corner value within its rounding
+// bound of 0 is decided exactly: (b-a) x (c-a) = a x b + b x c + c x a is a sum
+// of 6 products of input doubles, accumulated in the K5 long accumulator.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ int exact_orient2d(double ax, double ay, double bx, double by, double cx, double cy) {
+    uint64_t acc[KW];
+#pragma unroll 1
+    for (int q = 0; q < KW; ++q) acc[q] = 0;
+    kulisch_add(acc, ax, by, 1.0, 1);
+    kulisch_add(acc, ay, bx, 1.0, -1);
+    kulisch_add(acc, bx, cy, 1.0, 1);
+    kulisch_add(acc, by, cx, 1.0, -1);
+    kulisch_add(acc, cx, ay, 1.0, 1);
+    kulisch_add(acc, cy, ax, 1.0, -1);
+    return kulisch_sign(acc);
+}
+
+__global__ void __launch_bounds__(256) quad_kernel(const double* __restrict__ coords, int64_t n,
+                                                    uint8_t* __restrict__ flags, double* __restrict__ J_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double q[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) q[p] = __ldcs(coords + (int64_t)p * n + i);
+    bool bad = false;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) bad |= !(fabs(q[p]) <= 0x1p300);
+    uint8_t f;
+    double J[4];
+    if (bad) {
+        f = HEXVAL_NONFINITE;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) J[k] = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+        const double v12x = __dsub_rn(q[2], q[0]), v12y = __dsub_rn(q[3], q[1]);
+        const double v43x = __dsub_rn(q[4], q[6]), v43y = __dsub_rn(q[5], q[7]);
+        const double v14x = __dsub_rn(q[6], q[0]), v14y = __dsub_rn(q[7], q[1]);
+        const double v23x = __dsub_rn(q[4], q[2]), v23y = __dsub_rn(q[5], q[3]);
+        // corner k: J_k = u x w (reading Q1: J3 at (1,1) pairs v43 with v23)
+        const double ux[4] = {v12x, v12x, v43x, v43x}, uy[4] = {v12y, v12y, v43y, v43y};
+        const double wx[4] = {v14x, v23x, v23x, v14x}, wy[4] = {v14y, v23y, v23y, v14y};
+        // (origin, xi-neighbour, eta-neighbour) of each corner as an orientation of input points
+        const int o[4][3] = {{0, 1, 3}, {0, 1, 2}, {2, 3, 1}, {3, 0, 2}};
+        bool valid = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double a = __dmul_rn(ux[k], wy[k]), b = __dmul_rn(uy[k], wx[k]);
+            J[k] = __dsub_rn(a, b);
+            // |fl(J) - J| <= 8 u (|a| + |b|) for inputs with rounded differences (+ underflow)
+            const double tau = __fma_rn(8.0 * U_ROUND, __dadd_rn(fabs(a), fabs(b)), 0x1p-1060);
+            if (J[k] < -tau) valid = false;
+            else if (!(J[k] > tau) && valid)
+                valid = exact_orient2d(q[2 * o[k][0]], q[2 * o[k][0] + 1], q[2 * o[k][1]], q[2 * o[k][1] + 1],
+                                       q[2 * o[k][2]], q[2 * o[k][2] + 1]) > 0;
+        }
+        f = valid ? HEXVAL_VALID : HEXVAL_INVALID;
+    }
+    __stcs(flags + i, f);
+    if (J_out)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) __stcs(J_out + (int64_t)k * n + i, J[k]);
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 struct DeviceInfo {
@@ -1518,6 +1697,41 @@ int hexval_min_detj_bounds_indexed(const double* vertices, const int32_t* hex_id
         return HEXVAL_ERR_ALIGNMENT;
     return run_bounds(IdxLoader{vertices, hex_idx}, n, rel_tol, lower_out, upper_out, status_out_opt, nodes_dev_opt,
                       stream);
+}
+
+int hexval_select_valid(const uint8_t* flags, int64_t n, const int32_t* group_opt, int64_t n_groups,
+                        int32_t* ids_out_opt, long long* count_dev, int32_t* group_counts_opt, cudaStream_t stream) {
+    if (n < 0 || n > INT32_MAX || n_groups < 0) return HEXVAL_ERR_ARGUMENT;
+    if (!count_dev || (n > 0 && !flags) || ((group_opt == nullptr) != (group_counts_opt == nullptr)))
+        return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(count_dev, 8) || misaligned(ids_out_opt, 4) || misaligned(group_opt, 4) ||
+        misaligned(group_counts_opt, 4))
+        return HEXVAL_ERR_ALIGNMENT;
+    if (n == 0) {
+        cudaMemsetAsync(count_dev, 0, sizeof(long long), stream);
+        return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
+    }
+    const int64_t tiles = (n + SEL_TILE - 1) / SEL_TILE;
+    unsigned* tc = nullptr;
+    if (cudaMallocAsync((void**)&tc, (size_t)tiles * sizeof(unsigned), stream) != cudaSuccess) {
+        cudaGetLastError();
+        return HEXVAL_ERR_ALLOC;
+    }
+    select_count_kernel<<<(unsigned)tiles, SEL_THREADS, 0, stream>>>(flags, n, group_opt, group_counts_opt, tc);
+    select_scan_kernel<<<1, 1024, 0, stream>>>(tc, tiles, count_dev);
+    if (ids_out_opt) select_write_kernel<<<(unsigned)tiles, SEL_THREADS, 0, stream>>>(flags, n, tc, ids_out_opt);
+    cudaFreeAsync(tc, stream);
+    return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
+}
+
+int hexval_check_quad_soa(const double* coords, int64_t n, uint8_t* flags_out, double* J_out_opt,
+                          cudaStream_t stream) {
+    if (n < 0 || n > INT32_MAX) return HEXVAL_ERR_ARGUMENT;
+    if (n > 0 && (!coords || !flags_out)) return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(coords, 8) || misaligned(J_out_opt, 8)) return HEXVAL_ERR_ALIGNMENT;
+    if (n == 0) return HEXVAL_OK;
+    quad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(coords, n, flags_out, J_out_opt);
+    return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
 }
 
 int hexval_check_soa(const double* coords, int64_t n, uint8_t* flags_out, double* coeffs_out_opt,

@@ -485,3 +485,81 @@ def test_min_detj_bounds_closed_forms(golden_hexes):
     assert np.isnan(lo[m + 2]) and st[m + 2] == 2
     assert up[m + 3] < 0 and lo[m + 4] > 0 and up[m + 5] < 0      # Figs. 5, 6, 7
     assert int(nodes.item()) > 0
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: candidate-set filtering
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [0, 1, 4095, 4096, 4097, 1_000_003])
+def test_select_valid_parity(n):
+    rng = np.random.default_rng(n)
+    flags = rng.choice(np.array([0, 1, 2, 3, 5, 6], np.uint8), size=n, p=[.3, .4, .05, .05, .1, .1])
+    group = rng.integers(0, 1000, size=n).astype(np.int32)
+    f = torch.from_numpy(flags).cuda()
+    g = torch.from_numpy(group).cuda()
+    ids, c, counts = hv.select_valid(f, g, 1000)
+    torch.cuda.synchronize()
+    ref_ids, ref_counts = oracle.select_valid(flags, group, 1000)
+    assert c == ref_ids.size
+    assert np.array_equal(ids.cpu().numpy(), ref_ids)
+    assert np.array_equal(counts.cpu().numpy(), ref_counts)
+    if n > 1:                                   # misaligned flags view (scalar path)
+        ids2, c2, _ = hv.select_valid(f[1:])
+        torch.cuda.synchronize()
+        assert np.array_equal(ids2.cpu().numpy(), oracle.select_valid(flags[1:])[0])
+
+
+def test_select_valid_config3_pipeline():
+    """The paper's motivating pipeline on a config-3 slice: check candidates, keep the valid
+    ones, count valid candidates per grid cell (candidate h uses cell h mod 99^3)."""
+    start, count = 5_000_000, 2_000_000
+    verts, idx = hexgen.indexed_config(3, start=start, count=count)
+    f, _ = gpu_indexed(verts, idx)
+    cells = ((np.arange(start, start + count) % (99 ** 3))).astype(np.int32)
+    ids, c, counts = hv.select_valid(torch.from_numpy(f).cuda(), torch.from_numpy(cells).cuda(), 99 ** 3)
+    torch.cuda.synchronize()
+    ref_ids, ref_counts = oracle.select_valid(f, cells, 99 ** 3)
+    assert np.array_equal(ids.cpu().numpy(), ref_ids) and np.array_equal(counts.cpu().numpy(), ref_counts)
+    sel = np.random.default_rng(3).choice(count, 20000, replace=False)
+    ref = oracle.check_indexed(verts, idx[sel])
+    assert_flags_match(f[sel], ref)
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: linear quadrangles
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 255, 257, 100_003])
+def test_quad_parity(n):
+    coords = hexgen.quad_soa(n, 0.45, seed=n)
+    f, J = hv.check_quad_soa(torch.from_numpy(coords).cuda(), J=True)
+    torch.cuda.synchronize()
+    f, J = f.cpu().numpy(), J.cpu().numpy()
+    ref = oracle.check_quad_soa(coords)
+    assert np.array_equal(f, ref["flags"])                    # exact signs on both sides: no exclusions
+    assert np.array_equal(J, ref["J"])                        # same two products and difference
+    assert np.any(f == hv.INVALID) and np.any(f == hv.VALID)
+
+
+def test_quad_degenerate_and_special():
+    """Collinear / coincident nodes (exact zeros decided exactly), NaN, bowtie, chevron."""
+    rng = np.random.default_rng(71)
+    Q = [hexgen.UNIT_SQUARE, hexgen.UNIT_SQUARE[[0, 1, 3, 2]], np.array([[0, 0], [2, 0], [1, .5], [0, 2]], float)]
+    for _ in range(2000):
+        P = np.round((hexgen.UNIT_SQUARE + rng.uniform(-0.5, 0.5, size=(4, 2))) * 4) / 4   # dyadic grid: many zeros
+        if rng.random() < 0.3:
+            i, j = rng.choice(4, 2, replace=False)
+            P[j] = P[i]
+        Q.append(P)
+    N = hexgen.UNIT_SQUARE.copy(); N[1, 1] = np.nan
+    Q.append(N)
+    Q = np.stack(Q)
+    coords = np.ascontiguousarray(Q.reshape(len(Q), 8).T)
+    f, _ = hv.check_quad_soa(torch.from_numpy(coords).cuda())
+    torch.cuda.synchronize()
+    f = f.cpu().numpy()
+    ref = oracle.check_quad_soa(coords)
+    assert np.array_equal(f, ref["flags"])
+    assert f[0] == hv.VALID and f[1] == hv.INVALID and f[2] == hv.INVALID and f[-1] == hv.NONFINITE
+    assert ref["near"].sum() > 100                             # the exact path was exercised

@@ -508,3 +508,93 @@ def test_bounds_against_dense_sampling_and_verdicts():
                 assert (flags["flags"] & 3) == oracle.VALID
             if res["upper"] <= 0:
                 assert (flags["flags"] & 3) == oracle.INVALID
+
+
+def test_select_valid_brute_force():
+    """NEXT-3 oracle against a plain loop on small inputs (all flag values, empty groups)."""
+    rng = np.random.default_rng(51)
+    for n in (0, 1, 17, 1000):
+        flags = rng.choice(np.array([0, 1, 2, 3, 4, 5, 6], np.uint8), size=n)
+        group = rng.integers(0, 7, size=n).astype(np.int32)
+        ids, counts = oracle.select_valid(flags, group, 9)
+        exp_ids = [i for i in range(n) if flags[i] & 3 == 1]
+        exp_counts = [sum(1 for i in exp_ids if group[i] == g) for g in range(9)]
+        assert ids.tolist() == exp_ids and counts.tolist() == exp_counts
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: linear quadrangle (PAPER.md:282-349)
+# --------------------------------------------------------------------------
+
+SQ = np.array([[0, 0], [1, 0], [1, 1], [0, 1]], dtype=np.float64)
+
+
+def _quad_detj(Q, xi, eta):
+    """det J of the bilinear map from the shape functions of PAPER.md:290-297 (independent)."""
+    xi = np.asarray(xi, dtype=np.float64)[..., None]
+    eta = np.asarray(eta, dtype=np.float64)[..., None]
+    dxi = -(1 - eta) * Q[0] + (1 - eta) * Q[1] + eta * Q[2] - eta * Q[3]
+    deta = -(1 - xi) * Q[0] - xi * Q[1] + xi * Q[2] + (1 - xi) * Q[3]
+    return dxi[..., 0] * deta[..., 1] - dxi[..., 1] * deta[..., 0]
+
+
+def test_quad_special_cases():
+    """Unit square valid; bowtie (nodes 3, 4 swapped: self-intersecting) and chevron
+    (non-convex: one corner reflex) invalid; a mirrored square is invalid."""
+    assert oracle.check_quad(SQ)["flags"] == oracle.VALID
+    assert np.array_equal(oracle.check_quad(SQ)["J"], [1, 1, 1, 1])
+    assert oracle.check_quad(SQ[[0, 1, 3, 2]])["flags"] == oracle.INVALID
+    chevron = np.array([[0, 0], [2, 0], [1, 0.5], [0, 2]], dtype=np.float64)
+    assert oracle.check_quad(chevron)["flags"] == oracle.INVALID
+    assert oracle.check_quad(SQ * [-1, 1])["flags"] == oracle.INVALID
+    bad = SQ.copy(); bad[2, 0] = np.nan
+    assert oracle.check_quad(bad)["flags"] == oracle.NONFINITE
+
+
+def test_quad_corner_values_identity_and_areas():
+    """J_k = det J at corner k = twice the signed area of the corner triangle, and
+    J1 + J3 = J2 + J4; affine quads have four equal values."""
+    rng = np.random.default_rng(61)
+    corners = [(0, 0), (1, 0), (1, 1), (0, 1)]
+    tri = [(0, 1, 3), (1, 2, 0), (2, 3, 1), (3, 0, 2)]       # corner k and its two neighbours, ccw
+    for _ in range(300):
+        Q = SQ + rng.uniform(-0.4, 0.4, size=(4, 2))
+        r = oracle.check_quad(Q)
+        for k in range(4):
+            assert abs(r["J"][k] - _quad_detj(Q, *corners[k])) <= 1e-14
+            a, b, c = Q[list(tri[k])]
+            area2 = (b[0] - a[0]) * (c[1] - a[1]) - (b[1] - a[1]) * (c[0] - a[0])
+            assert abs(r["J"][k] - area2) <= 1e-14
+        J = r["J"]
+        assert abs(J[0] + J[2] - J[1] - J[3]) <= 1e-14
+        A = rng.normal(size=(2, 2))
+        P = SQ @ A.T + rng.normal(size=2)
+        assert np.allclose(oracle.check_quad(P)["J"], np.linalg.det(A), atol=1e-14)
+
+
+def test_quad_brute_force_and_exact_orientation():
+    """Dense sampling never contradicts a verdict (det J is bilinear: its minimum is a
+    corner value); the exact orientation sign agrees with Python rationals, including
+    collinear (exactly zero) configurations, which are INVALID (reading G2)."""
+    rng = np.random.default_rng(62)
+    t = np.linspace(0, 1, 21)
+    XI, ETA = np.meshgrid(t, t, indexing="ij")
+    for _ in range(300):
+        Q = SQ + rng.uniform(-0.6, 0.6, size=(4, 2))
+        r = oracle.check_quad(Q)
+        v = _quad_detj(Q, XI, ETA)
+        if r["flags"] == oracle.VALID:
+            assert v.min() > -1e-14
+        else:
+            assert min(r["J"]) <= 1e-14
+    for _ in range(200):
+        a = rng.integers(-4, 5, size=2) / 8.0
+        d = rng.integers(-4, 5, size=2) / 8.0
+        b = a + d
+        c = a + d * rng.integers(-3, 4)                         # collinear with a, b
+        for p, q, s in ((a, b, c), (a, b, rng.normal(size=2))):
+            ex = (Fraction(q[0]) - Fraction(p[0])) * (Fraction(s[1]) - Fraction(p[1])) - \
+                 (Fraction(q[1]) - Fraction(p[1])) * (Fraction(s[0]) - Fraction(p[0]))
+            assert oracle.exact_orient2d(p, q, s) == (ex > 0) - (ex < 0)
+    Q = SQ.copy(); Q[2] = [1.0, 0.0]                             # node 3 on node 2: J2 = J3 = 0 exactly
+    assert oracle.check_quad(Q)["flags"] == oracle.INVALID
