@@ -47,6 +47,7 @@ struct Ctl {                 // per-call control block (device scratch)
 // loaders: SoA planes or indexed gather
 // ---------------------------------------------------------------------------
 struct SoaLoader {
+    static constexpr bool kIntStep2 = false;     // see step2_class
     const double* __restrict__ coords;
     int64_t n;
     // pass 1: streamed once, evict-first
@@ -63,6 +64,7 @@ struct SoaLoader {
 };
 
 struct IdxLoader {
+    static constexpr bool kIntStep2 = true;      // see step2_class
     const double* __restrict__ verts;
     const int32_t* __restrict__ idx;
     __device__ __forceinline__ void load(int64_t i, double* X) const {
@@ -143,6 +145,13 @@ __device__ __forceinline__ bool IdxLoader::dup_face_pair(int64_t i) const {
 // Step 2 classification shared by pass 1 and the exact kernel.
 enum : int { ST_INVALID = 0, ST_VALID = 1, ST_NONFINITE = 3, ST_SUB = 4, ST_EXACT = 5 };
 
+// INT_SLOW selects the slow path (some sample <= tau2 in its hi word): FP64
+// compares, or the integer pipe.  Measured on B200 with 3 interleaved A/B runs
+// (profiles/r01): FP64 compares are faster on SoA config 1 (337 vs 349 us; the
+// slow path is taken by ~80% of the warps there and the FP64 pipe has room),
+// the integer pipe on indexed config 3 (1606 vs 1795 us; 36% invalid hexes,
+// the FP64 pipe is the bottleneck).
+template <bool INT_SLOW>
 __device__ __forceinline__ int step2_class(const Samples& s, double tau2) {
     const int T = key(tau2);                          // tau2 > 0: key == abskey
     int km = key(s.c[0]);
@@ -151,20 +160,18 @@ __device__ __forceinline__ int step2_class(const Samples& s, double tau2) {
 #pragma unroll
     for (int e = 0; e < 12; ++e) km = min(km, key(s.d[e]));
     if (km > T) return ST_VALID;                       // every sample > tau2 > 0: robustly positive
-#ifndef HEXVAL_STEP2_INT
-    // slow path with FP64 compares (measured faster on config 1 than the
-    // integer-pipe variant below: 337 vs 349 us, 3 interleaved A/B runs)
-    bool neg = false, amb = false;
+    if (!INT_SLOW) {
+        bool neg = false, amb = false;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { neg |= s.c[k] < -tau2; amb |= fabs(s.c[k]) <= tau2; }
+        for (int k = 0; k < 8; ++k) { neg |= s.c[k] < -tau2; amb |= fabs(s.c[k]) <= tau2; }
 #pragma unroll
-    for (int e = 0; e < 12; ++e) { neg |= s.d[e] < -tau2; amb |= fabs(s.d[e]) <= tau2; }
-    if (neg) return ST_INVALID;
-    return amb ? ST_EXACT : ST_VALID;
-#endif
-    // Slow path on the integer pipe, conservative in the hi words: a sample is
-    // robustly negative if its sign is set and its hi word exceeds that of
-    // tau2 (then |x| > tau2); it is ambiguous if |x|'s hi word <= that of tau2.
+        for (int e = 0; e < 12; ++e) { neg |= s.d[e] < -tau2; amb |= fabs(s.d[e]) <= tau2; }
+        if (neg) return ST_INVALID;
+        return amb ? ST_EXACT : ST_VALID;
+    }
+    // Integer pipe, conservative in the hi words: a sample is robustly negative
+    // if its sign is set and its hi word exceeds that of tau2 (then |x| > tau2);
+    // it is ambiguous if |x|'s hi word <= that of tau2.
     unsigned um = 0;
     int am = 0x7fffffff;
 #pragma unroll
@@ -245,7 +252,7 @@ __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i
     } else {
         Samples s;
         samples20(X, s);                                  // S1 + S2
-        st = step2_class(s, step2_tau(s.ekey));           // S3 (Step 2)
+        st = step2_class<L::kIntStep2>(s, step2_tau(s.ekey));   // S3 (Step 2)
         if (st == ST_EXACT && ld.dup_face_pair(i)) st = ST_INVALID;   // a sample is exactly 0
         Coeffs t;
         transform(s, t);                                  // S4 (Step 3)
@@ -920,10 +927,58 @@ struct BWarp {
     int cnt[MAX_DEPTH + 1];
 };
 
+// Root phase of NEXT-1: one hex per thread; a hex whose root coefficients
+// already satisfy min(b) >= upper - tol is finished here, the others are
+// appended (warp-aggregated) to the queue the warp-cooperative kernel drains.
+__device__ __forceinline__ double root_bounds(const double* P, double rel_tol, double& up, double& mn) {
+    mn = P[0];
+    double sc_ = fabs(P[0]);
+#pragma unroll
+    for (int c = 1; c < 27; ++c) { mn = dmin(mn, P[c]); sc_ = fmax(sc_, fabs(P[c])); }
+    up = dmin(dmin(dmin(P[0], P[2]), dmin(P[6], P[8])), dmin(dmin(P[18], P[20]), dmin(P[24], P[26])));
+    return __dmul_rn(rel_tol, sc_);
+}
+
 template <class L>
-__global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, int64_t n, double rel_tol, double* __restrict__ lower_out,
+__global__ void __launch_bounds__(256) bounds_root_kernel(L ld, int64_t n, double rel_tol, double* __restrict__ lower_out,
+                                                           double* __restrict__ upper_out, uint8_t* __restrict__ status_out,
+                                                           unsigned* __restrict__ qcount, uint32_t* __restrict__ q) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool queue = false;
+    if (i < n) {
+        double X[24];
+        ld.load_stream(i, X);
+        double lo, up;
+        uint8_t st = 0;
+        if (out_of_range(X)) {
+            lo = up = __longlong_as_double(0x7ff8000000000000ll);
+            st = 2;                                          // NONFINITE
+        } else {
+            Samples smp;
+            samples20(X, smp);
+            Coeffs t;
+            transform(smp, t);
+            double P[27];
+            root_coeffs(smp, t, P);
+            double mn;
+            const double tol = root_bounds(P, rel_tol, up, mn);
+            lo = mn;
+            queue = !(mn >= up - tol);
+        }
+        if (!queue) {
+            __stcs(lower_out + i, lo);
+            __stcs(upper_out + i, up);
+            if (status_out) __stcs(status_out + i, st);
+        }
+    }
+    warp_append(queue, (uint32_t)i, q, qcount);
+}
+
+template <class L>
+__global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol, double* __restrict__ lower_out,
                                                             double* __restrict__ upper_out, uint8_t* __restrict__ status_out,
-                                                            unsigned* next, WarpStacks ws, unsigned long long* nodes_out) {
+                                                            unsigned* ctlq, const uint32_t* __restrict__ q, WarpStacks ws,
+                                                            unsigned long long* nodes_out) {
     __shared__ BWarp wst[K4_WARPS];
     const int lane = threadIdx.x & 31;
     BWarp& W = wst[threadIdx.x >> 5];
@@ -935,6 +990,7 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, int64_t n, dou
     __syncwarp();
     int top = 0, D = 0, nb = 0;
     unsigned long long nodes = 0;
+    const unsigned total = *((volatile unsigned*)&ctlq[0]);
     for (;;) {
         double P[27];
         bool act = false;
@@ -948,37 +1004,28 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, int64_t n, dou
                 if (status_out) status_out[h] = (uint8_t)W.capped[lane];
             }
             unsigned base = 0;
-            if (lane == 0) base = atomicAdd(next, 32u);
+            if (lane == 0) base = atomicAdd(&ctlq[1], 32u);
             base = __shfl_sync(0xffffffffu, base, 0);
-            nb = base < n ? (int)min((int64_t)32, n - (int64_t)base) : 0;
+            nb = base < total ? (int)min(32u, total - base) : 0;
             if (nb == 0) break;
             d = 0;
             if (lane < nb) {
-                const uint32_t h = base + lane;
+                const uint32_t h = q[base + lane];
                 W.hex[lane] = h;
                 W.capped[lane] = 0;
                 double X[24];
                 ld.load(h, X);
-                if (out_of_range(X)) {
-                    W.capped[lane] = 2;                      // NONFINITE: NaN bounds
-                    W.upper[lane] = W.lower[lane] = 0;
-                    W.tol[lane] = 0;
-                } else {
-                    Samples smp;
-                    samples20(X, smp);
-                    Coeffs t;
-                    transform(smp, t);
-                    root_coeffs(smp, t, P);
-                    double up = P[0], mn = P[0], sc_ = fabs(P[0]);
-#pragma unroll
-                    for (int c = 1; c < 27; ++c) { mn = dmin(mn, P[c]); sc_ = fmax(sc_, fabs(P[c])); }
-                    up = dmin(dmin(dmin(P[0], P[2]), dmin(P[6], P[8])), dmin(dmin(P[18], P[20]), dmin(P[24], P[26])));
-                    const double tol = __dmul_rn(rel_tol, sc_);
-                    W.tol[lane] = tol;
-                    W.upper[lane] = okey(up);
-                    W.lower[lane] = okey(mn >= up - tol ? mn : __longlong_as_double(0x7ff0000000000000ll));
-                    act = !(mn >= up - tol);                  // split the root
-                }
+                Samples smp;
+                samples20(X, smp);
+                Coeffs t;
+                transform(smp, t);
+                root_coeffs(smp, t, P);                      // bit-identical to the root phase
+                double up, mn;
+                const double tol = root_bounds(P, rel_tol, up, mn);
+                W.tol[lane] = tol;
+                W.upper[lane] = okey(up);
+                W.lower[lane] = okey(__longlong_as_double(0x7ff0000000000000ll));
+                act = true;                                  // queued: the root is split
             }
         } else {
             const int k = min(32, W.cnt[D]);
@@ -1595,24 +1642,24 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bounds_kernel<L>, K4_THREADS, 0);
     if (occ < 1) occ = 1;
-    const int64_t batches = (n + 31) / 32;
-    int64_t blocks = (int64_t)info.sms * occ;
-    const int64_t need = (batches + K4_WARPS - 1) / K4_WARPS;
-    if (need < blocks) blocks = need;
+    const int64_t blocks = (int64_t)info.sms * occ;
     const size_t warps = (size_t)blocks * K4_WARPS;
+    const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t sc_bytes = warps * 27 * K4_CAP * sizeof(double);
     const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
     char* base = nullptr;
-    if (cudaMallocAsync((void**)&base, 256 + sc_bytes + so_bytes, stream) != cudaSuccess) {
+    if (cudaMallocAsync((void**)&base, 256 + q_bytes + sc_bytes + so_bytes, stream) != cudaSuccess) {
         cudaGetLastError();
         return HEXVAL_ERR_ALLOC;
     }
-    unsigned* next = reinterpret_cast<unsigned*>(base);
+    unsigned* ctlq = reinterpret_cast<unsigned*>(base);          // [0] queue length, [1] fetch cursor
+    uint32_t* q = reinterpret_cast<uint32_t*>(base + 256);
     WarpStacks ws;
-    ws.coef = reinterpret_cast<double*>(base + 256);
-    ws.owner = reinterpret_cast<unsigned char*>(base + 256 + sc_bytes);
-    cudaMemsetAsync(next, 0, 256, stream);
-    bounds_kernel<L><<<(unsigned)blocks, K4_THREADS, 0, stream>>>(ld, n, rel_tol, lower, upper, status, next, ws,
+    ws.coef = reinterpret_cast<double*>(base + 256 + q_bytes);
+    ws.owner = reinterpret_cast<unsigned char*>(base + 256 + q_bytes + sc_bytes);
+    cudaMemsetAsync(ctlq, 0, 256, stream);
+    bounds_root_kernel<L><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(ld, n, rel_tol, lower, upper, status, ctlq, q);
+    bounds_kernel<L><<<(unsigned)blocks, K4_THREADS, 0, stream>>>(ld, rel_tol, lower, upper, status, ctlq, q, ws,
                                                                     nodes_dev_opt);
     cudaFreeAsync(base, stream);
     return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
