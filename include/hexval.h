@@ -67,7 +67,7 @@ typedef struct hexval_stats {
 /* Per-phase kernel timing (CUDA events recorded on the call's stream). */
 typedef struct hexval_profile hexval_profile;
 #define HEXVAL_PHASE_PASS1   0   /* pass-1 kernel: 20 dets, 27 coeffs, classify, compact */
-#define HEXVAL_PHASE_EXACT   1   /* exact-sign kernel for ambiguous root samples         */
+#define HEXVAL_PHASE_EXACT   1   /* exact signs: fused into the subdivision kernel, reads 0 */
 #define HEXVAL_PHASE_SUBDIV  2   /* subdivision kernel                                   */
 #define HEXVAL_NUM_PHASES    3
 

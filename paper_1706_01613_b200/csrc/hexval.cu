@@ -6,8 +6,9 @@
 //                        determinants, Step 2, 27 Bezier coefficients, Step 4,
 //                        flags, optional coefficients, and (K3) warp-ballot +
 //                        block-scan compaction of undecided / ambiguous hexes.
-//   K5    exact_kernel   exact signs of root samples within their rounding
-//                        bound of 0 (Kulisch accumulator), then Steps 3-4.
+//   K5    exact path     exact signs of root samples within their rounding
+//                        bound of 0 (Kulisch accumulator), then Steps 3-4;
+//                        drained by K4 while it fills its batches.
 //   K4    subdiv_kernel  persistent grid; each warp takes batches of 32 queued
 //                        hexes and splits up to 32 same-depth nodes per step
 //                        (one per lane), children pushed on a per-warp
@@ -30,7 +31,6 @@ using namespace hexval;
 namespace {
 
 constexpr int P1_THREADS = 256;
-constexpr int K5_THREADS = 128;
 constexpr int K4_THREADS = 128;
 
 // flags placeholders written by pass 1 for hexes that later kernels finish
@@ -40,7 +40,8 @@ struct Ctl {                 // per-call control block (device scratch)
     unsigned int n_sub;      // subdivision queue length
     unsigned int n_exact;    // exact-sign queue length
     unsigned int k4_next;    // dynamic fetch cursor of the subdivision kernel
-    unsigned int pad[5];
+    unsigned int ex_next;    // fetch cursor of the exact queue (drained by the subdivision kernel)
+    unsigned int pad[4];
 };
 
 // ---------------------------------------------------------------------------
@@ -618,36 +619,6 @@ __device__ __noinline__ uint8_t exact_resolve(const double* X) {
     return step4_positive(t) ? HEXVAL_VALID : HEXVAL_FLAG_SUBDIVIDED;
 }
 
-template <class L, bool STATS>
-__global__ void __launch_bounds__(K5_THREADS) exact_kernel(L ld, uint8_t* __restrict__ flags, Ctl* ctl,
-                                                           const uint32_t* __restrict__ qexact,
-                                                           uint32_t* __restrict__ qsub, hexval_stats* stats) {
-    const unsigned cnt = *((volatile unsigned*)&ctl->n_exact);
-    for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
-        const uint32_t h = qexact[q];
-        double X[24];
-        ld.load(h, X);
-        uint8_t f;
-        if (face_pair_coincident(X)) {
-            f = HEXVAL_INVALID;                          // a Step-2 sample is exactly 0
-        } else {
-            f = exact_resolve(X);
-            if (f == HEXVAL_FLAG_SUBDIVIDED) qsub[atomicAdd(&ctl->n_sub, 1u)] = h;
-        }
-        flags[h] = f;
-        if (STATS) {                                     // warp-aggregated counters
-            const unsigned am = __activemask();
-            const unsigned ninv = __popc(__ballot_sync(am, f == HEXVAL_INVALID));
-            const unsigned nval = __popc(__ballot_sync(am, f == HEXVAL_VALID));
-            if ((threadIdx.x & 31) == (unsigned)(__ffs(am) - 1)) {
-                atomicAdd(&stats->n_exact, (unsigned long long)__popc(am));
-                if (ninv) atomicAdd(&stats->n_invalid, (unsigned long long)ninv);
-                if (nval) atomicAdd(&stats->n_valid, (unsigned long long)nval);
-            }
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
 // K4: recursive_subdivision, depth-first per thread
 // ---------------------------------------------------------------------------
@@ -740,6 +711,12 @@ struct CoordRoot {
         transform(s, t);
         root_coeffs(s, t, P);
     }
+    // K5 fused into K4: Steps 2-4 of an ambiguous hex with exact signs
+    __device__ __forceinline__ uint8_t exact(uint32_t h) const {
+        double X[24];
+        ld.load(h, X);
+        return face_pair_coincident(X) ? (uint8_t)HEXVAL_INVALID : exact_resolve(X);
+    }
 };
 
 struct CoeffRoot {
@@ -749,11 +726,13 @@ struct CoeffRoot {
 #pragma unroll
         for (int sg = 0; sg < 27; ++sg) P[kSigmaToSlot[sg]] = __ldg(b + (int64_t)sg * n + h);
     }
+    __device__ __forceinline__ uint8_t exact(uint32_t) const { return HEXVAL_FLAG_SUBDIVIDED; }   // no exact queue
 };
 
 template <class R, bool STATS, int MINB>
 __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
-                                                            const uint32_t* __restrict__ qsub, WarpStacks ws,
+                                                            const uint32_t* __restrict__ qsub,
+                                                            const uint32_t* __restrict__ qexact, WarpStacks ws,
                                                             hexval_stats* stats) {
     __shared__ K4Warp wst[K4_WARPS];
     const int lane = threadIdx.x & 31;
@@ -762,11 +741,12 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
     double* const sc = ws.coef + gw * 27 * K4_CAP;
     unsigned char* const so = ws.owner + gw * K4_CAP;
     const unsigned total = *((volatile unsigned*)&ctl->n_sub);
+    const unsigned n_exact = *((volatile unsigned*)&ctl->n_exact);
     const unsigned lt_mask = (1u << lane) - 1u;
     if (lane <= MAX_DEPTH) W.cnt[lane] = 0;
     __syncwarp();
     int top = 0, D = 0, nb = 0;                         // warp-uniform: stack size, top level, batch size
-    unsigned long long nodes = 0, n_inv = 0, n_val = 0, n_und = 0;
+    unsigned long long nodes = 0, n_inv = 0, n_val = 0, n_und = 0, n_ex = 0, n_exi = 0, n_exv = 0;
     int maxd = 0;
     for (;;) {
         double P[27];
@@ -780,18 +760,48 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
                 flags[W.hex[lane]] = v | HEXVAL_FLAG_SUBDIVIDED;
                 if (STATS) { n_inv += v == HEXVAL_INVALID; n_val += v == HEXVAL_VALID; n_und += v == HEXVAL_UNDETERMINED; }
             }
-            unsigned base = 0;
-            if (lane == 0) base = atomicAdd(&ctl->k4_next, 32u);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            nb = base < total ? (int)min(32u, total - base) : 0;
+            // fill the next batch: first ambiguous hexes from the exact queue (K5 fused
+            // here: each lane resolves one; the undecided ones join this warp's batch,
+            // and at most as many are claimed as there are free slots), then hexes
+            // pass 1 left undecided
+            nb = 0;
+            while (nb < 32) {
+                const unsigned want = 32u - (unsigned)nb;
+                unsigned eb = 0;
+                if (lane == 0) eb = atomicAdd(&ctl->ex_next, want);
+                eb = __shfl_sync(0xffffffffu, eb, 0);
+                const unsigned got = eb < n_exact ? min(want, n_exact - eb) : 0u;
+                if (got == 0) break;
+                bool sub = false;
+                uint32_t h = 0;
+                if ((unsigned)lane < got) {
+                    h = qexact[eb + lane];
+                    const uint8_t f = root.exact(h);
+                    if (f == HEXVAL_FLAG_SUBDIVIDED) sub = true;
+                    else flags[h] = f;
+                    if (STATS) { ++n_ex; n_exi += f == HEXVAL_INVALID; n_exv += f == HEXVAL_VALID; }
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, sub);
+                if (sub) W.hex[nb + __popc(bal & lt_mask)] = h;
+                nb += __popc(bal);
+                if (got < want) break;
+            }
+            if (nb < 32) {
+                unsigned base = 0;
+                const unsigned want = 32u - (unsigned)nb;
+                if (lane == 0) base = atomicAdd(&ctl->k4_next, want);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const unsigned got = base < total ? min(want, total - base) : 0u;
+                if ((unsigned)lane >= (unsigned)nb && (unsigned)lane < nb + got) W.hex[lane] = qsub[base + lane - nb];
+                nb += (int)got;
+            }
+            __syncwarp();
             if (nb == 0) break;
             act = lane < nb;
             d = 0;
             if (act) {
-                const uint32_t h = qsub[base + lane];
-                W.hex[lane] = h;
                 W.status[lane] = 0;
-                root(h, P);                              // bit-identical to pass 1
+                root(W.hex[lane], P);                    // bit-identical to pass 1
             }
         } else {
             const int k = min(32, W.cnt[D]);
@@ -885,6 +895,14 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
             n_inv += __shfl_xor_sync(0xffffffffu, n_inv, o);
             n_val += __shfl_xor_sync(0xffffffffu, n_val, o);
             n_und += __shfl_xor_sync(0xffffffffu, n_und, o);
+            n_ex += __shfl_xor_sync(0xffffffffu, n_ex, o);
+            n_exi += __shfl_xor_sync(0xffffffffu, n_exi, o);
+            n_exv += __shfl_xor_sync(0xffffffffu, n_exv, o);
+        }
+        if (lane == 0 && n_ex) {
+            atomicAdd(&stats->n_exact, n_ex);
+            if (n_exi) atomicAdd(&stats->n_invalid, n_exi);
+            if (n_exv) atomicAdd(&stats->n_valid, n_exv);
         }
         if (lane == 0) {
             const unsigned long long nsub = n_inv + n_val + n_und;
@@ -1495,19 +1513,21 @@ void launch_pass1<SoaLoader>(const SoaLoader& ld, const DeviceInfo& info, int64_
 
 template <class R>
 void launch_subdiv(const R& root, const DeviceInfo& info, unsigned blocks, uint8_t* flags, Ctl* ctl,
-                   const uint32_t* qsub, const WarpStacks& fr, hexval_stats* stats, cudaStream_t stream) {
+                   const uint32_t* qsub, const uint32_t* qex, const WarpStacks& fr, hexval_stats* stats,
+                   cudaStream_t stream) {
     if (info.k4_minb == 3) {
-        if (stats) subdiv_kernel<R, true, 3><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
-        else subdiv_kernel<R, false, 3><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
+        if (stats) subdiv_kernel<R, true, 3><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
+        else subdiv_kernel<R, false, 3><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
     } else {
-        if (stats) subdiv_kernel<R, true, 2><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
-        else subdiv_kernel<R, false, 2><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, fr, stats);
+        if (stats) subdiv_kernel<R, true, 2><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
+        else subdiv_kernel<R, false, 2><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
     }
 }
 
 int collect_profile(hexval_profile* p) {
     for (int k = 0; k < p->count; ++k)
         for (int ph = 0; ph < HEXVAL_NUM_PHASES; ++ph) {
+            if (ph == HEXVAL_PHASE_EXACT) continue;          // fused into the subdivision kernel
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, p->ev[k][ph][0], p->ev[k][ph][1]) != cudaSuccess) return HEXVAL_ERR_CUDA;
             p->pending_ms[ph] += ms;
@@ -1553,15 +1573,11 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     mark(HEXVAL_PHASE_PASS1, 0);
     launch_pass1(ld, info, n, flags, coeffs, ctl, qsub, qex, stats, stream);
     mark(HEXVAL_PHASE_PASS1, 1);
-    mark(HEXVAL_PHASE_EXACT, 0);
-    const unsigned k5_blocks = (unsigned)info.sms * 8;
-    if (stats) exact_kernel<L, true><<<k5_blocks, K5_THREADS, 0, stream>>>(ld, flags, ctl, qex, qsub, stats);
-    else exact_kernel<L, false><<<k5_blocks, K5_THREADS, 0, stream>>>(ld, flags, ctl, qex, qsub, stats);
-    mark(HEXVAL_PHASE_EXACT, 1);
+    // K5 (exact signs) is fused into K4's batch filling: no separate launch
     mark(HEXVAL_PHASE_SUBDIV, 0);
     const unsigned k4_blocks = (unsigned)(info.sms * info.k4_blocks_per_sm);
     const CoordRoot<L> root{ld};
-    launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, fr, stats, stream);
+    launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, qex, fr, stats, stream);
     mark(HEXVAL_PHASE_SUBDIV, 1);
     cudaFreeAsync(base, stream);
     if (cudaGetLastError() != cudaSuccess) return HEXVAL_ERR_CUDA;
@@ -1626,7 +1642,7 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     else bezier_pass_kernel<false><<<p1_blocks, P1_THREADS, 0, stream>>>(b, n, flags, ctl, qsub, stats);
     const CoeffRoot root{b, n};
     const unsigned k4_blocks = (unsigned)(info.sms * info.k4_blocks_per_sm);
-    launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, fr, stats, stream);
+    launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, qsub, fr, stats, stream);
     cudaFreeAsync(base, stream);
     if (cudaGetLastError() != cudaSuccess) return HEXVAL_ERR_CUDA;
     return HEXVAL_OK;
@@ -1748,16 +1764,15 @@ int hexval_min_detj_bounds_indexed(const double* vertices, const int32_t* hex_id
 
 int hexval_select_valid(const uint8_t* flags, int64_t n, const int32_t* group_opt, int64_t n_groups,
                         int32_t* ids_out_opt, long long* count_dev, int32_t* group_counts_opt, cudaStream_t stream) {
-    if (n < 0 || n > INT32_MAX || n_groups < 0) return HEXVAL_ERR_ARGUMENT;
-    if (!count_dev || (n > 0 && !flags) || ((group_opt == nullptr) != (group_counts_opt == nullptr)))
-        return HEXVAL_ERR_ARGUMENT;
-    if (misaligned(count_dev, 8) || misaligned(ids_out_opt, 4) || misaligned(group_opt, 4) ||
-        misaligned(group_counts_opt, 4))
-        return HEXVAL_ERR_ALIGNMENT;
-    if (n == 0) {
+    if (n < 0 || n > INT32_MAX || n_groups < 0 || !count_dev) return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(count_dev, 8)) return HEXVAL_ERR_ALIGNMENT;
+    if (n == 0) {                                     // nothing to select (empty arrays may be NULL)
         cudaMemsetAsync(count_dev, 0, sizeof(long long), stream);
         return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
     }
+    if (!flags || ((group_opt == nullptr) != (group_counts_opt == nullptr))) return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(ids_out_opt, 4) || misaligned(group_opt, 4) || misaligned(group_counts_opt, 4))
+        return HEXVAL_ERR_ALIGNMENT;
     const int64_t tiles = (n + SEL_TILE - 1) / SEL_TILE;
     unsigned* tc = nullptr;
     if (cudaMallocAsync((void**)&tc, (size_t)tiles * sizeof(unsigned), stream) != cudaSuccess) {
@@ -1965,6 +1980,6 @@ const char* hexval_status_string(int status) {
 
 int hexval_version(void) { return 100; }
 
-int hexval_kernel_launches_per_call(void) { return 3; }
+int hexval_kernel_launches_per_call(void) { return 2; }
 
 }  // extern "C"
