@@ -30,7 +30,7 @@ __all__ = [
 INVALID, VALID, UNDETERMINED, NONFINITE = 0, 1, 2, 3
 FLAG_SUBDIVIDED = 4
 MAX_DEPTH = 20
-PHASES = ("pass1", "exact", "subdiv")
+PHASES = ("pass1", "exact", "subdiv")          # "exact" is fused into "subdiv" (reads 0)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # HEXVAL_LIB selects an in-tree variant build (A/B measurements); default libhexval.so

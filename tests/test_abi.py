@@ -45,7 +45,7 @@ def test_status_strings(L):
     for code in (-1, -2, -3, -4):
         assert hv.status_string(code) != "unknown status"
     assert hv.version() >= 100
-    assert hv.kernel_launches_per_call() == 3
+    assert hv.kernel_launches_per_call() == 2            # pass 1 + subdivision (exact path fused)
 
 
 def test_argument_errors_without_gpu(L):
