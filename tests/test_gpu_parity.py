@@ -564,3 +564,38 @@ def test_quad_degenerate_and_special():
     assert np.array_equal(f, ref["flags"])
     assert f[0] == hv.VALID and f[1] == hv.INVALID and f[2] == hv.INVALID and f[-1] == hv.NONFINITE
     assert ref["near"].sum() > 100                             # the exact path was exercised
+
+
+# --------------------------------------------------------------------------
+# properties of the CUDA path that hold at any size (checked without the oracle)
+# --------------------------------------------------------------------------
+
+def test_power_of_two_scaling_and_translation_invariance():
+    """Scaling all coordinates by 2^k scales every det J value, and so every computed
+    coefficient, by exactly 8^k (no rounding changes); verdicts are unchanged.  A
+    translation by a small dyadic vector changes rounding only: verdicts of hexes the
+    oracle does not mark near-boundary are unchanged."""
+    coords = hexgen.ragged_soa(50_000, seed=81, amp=0.45)
+    f0, k0 = gpu_soa(coords, coeffs=True)
+    for s in (2.0 ** -30, 2.0 ** 7):
+        f, k = gpu_soa(coords * s, coeffs=True)
+        assert np.array_equal(f, f0)
+        assert np.array_equal(k, k0 * s ** 3)
+    ref = oracle.check_soa(coords)
+    ft, _ = gpu_soa(coords + 0.125)
+    sure = ref["near"] == 0
+    assert np.array_equal(ft[sure], f0[sure])
+
+
+def test_node_relabelling_by_cube_rotation_preserves_verdict():
+    """A proper rotation of the reference cube relabels the nodes (det J composed with an
+    orientation-preserving map of [0,1]^3): validity is unchanged."""
+    coords = hexgen.ragged_soa(20_000, seed=82, amp=0.45)
+    X = hexgen.soa_to_nodes(coords)
+    f0, _ = gpu_soa(coords)
+    ref = oracle.check_soa(coords)
+    sure = ref["near"] == 0
+    # rotation by 90 degrees about zeta: node k -> image of its reference corner
+    perm = [1, 2, 3, 0, 5, 6, 7, 4]
+    f1, _ = gpu_soa(hexgen.nodes_to_soa(X[:, perm]))
+    assert np.array_equal((f1 & 3)[sure], (f0 & 3)[sure])
