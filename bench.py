@@ -345,6 +345,7 @@ def run_ours(args, world, rank, local):
         "nodes_per_step": st["n_nodes"],
         "subdiv_kernel_ms": subdiv_ms,
         "nodes_per_s": (st["n_nodes"] / (subdiv_ms * 1e-3)) if subdiv_ms > 0 and st["n_nodes"] else None,
+        "lane_use": (st["n_nodes"] / st["n_lane_steps"]) if st.get("n_lane_steps") else None,
         "fp64_ops_per_node": FP64_OPS_PER_NODE,
         "fp64_achieved_gops": (st["n_nodes"] * FP64_OPS_PER_NODE / (subdiv_ms * 1e-3) / 1e9) if subdiv_ms > 0 and st["n_nodes"] else None,
         "fp64_peak_gops_at_max_clock": FP64_PEAK_GOPS,

@@ -62,6 +62,8 @@ typedef struct hexval_stats {
     unsigned long long n_exact;          /* hexes whose Step 2 needed exact signs */
     unsigned long long n_nodes;          /* recursive_subdivision calls     */
     unsigned long long max_depth;        /* deepest child depth classified  */
+    unsigned long long n_lane_steps;     /* subdivision kernel: 32 x warp steps (lane slots
+                                            offered); n_nodes / n_lane_steps = lane use */
 } hexval_stats;
 
 /* Per-phase kernel timing (CUDA events recorded on the call's stream). */

@@ -146,7 +146,7 @@ class Stats:
     """Device-side counters (``hexval_stats``) accumulated by the *_ex calls."""
 
     FIELDS = ("n_valid", "n_invalid", "n_undetermined", "n_nonfinite", "n_subdivided",
-              "n_exact", "n_nodes", "max_depth")
+              "n_exact", "n_nodes", "max_depth", "n_lane_steps")
 
     def __init__(self, device=None):
         torch = _torch()

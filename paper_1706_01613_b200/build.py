@@ -48,6 +48,19 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     return target
 
 
+DEBUG_LIB = os.path.join(HERE, "libhexval_debug.so")
+
+
+def build_all(force: bool = False) -> list[str]:
+    """The product library and its HEXVAL_DEBUG variant (invariant traps; used by the GPU tests)."""
+    out = [build(force=force)]
+    if force or not os.path.exists(DEBUG_LIB) or any(os.path.getmtime(d) > os.path.getmtime(DEBUG_LIB) for d in DEPS):
+        out.append(build(out=DEBUG_LIB, defines=("HEXVAL_DEBUG",)))
+    else:
+        out.append(DEBUG_LIB)
+    return out
+
+
 if __name__ == "__main__":
     import argparse
     ap = argparse.ArgumentParser()

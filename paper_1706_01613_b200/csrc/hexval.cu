@@ -28,6 +28,20 @@
 
 using namespace hexval;
 
+// Debug builds (-DHEXVAL_DEBUG, e.g. `build.py --out libhexval_debug.so -D HEXVAL_DEBUG`)
+// trap on any violated capacity / index invariant; compute-sanitizer is not
+// available on the GPU pool, so the GPU tests are also run against that build.
+#ifdef HEXVAL_DEBUG
+#define HV_CHECK(cond) \
+    do {               \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define HV_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 namespace {
 
 constexpr int P1_THREADS = 256;
@@ -746,7 +760,7 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
     if (lane <= MAX_DEPTH) W.cnt[lane] = 0;
     __syncwarp();
     int top = 0, D = 0, nb = 0;                         // warp-uniform: stack size, top level, batch size
-    unsigned long long nodes = 0, n_inv = 0, n_val = 0, n_und = 0, n_ex = 0, n_exi = 0, n_exv = 0;
+    unsigned long long nodes = 0, n_inv = 0, n_val = 0, n_und = 0, n_ex = 0, n_exi = 0, n_exv = 0, steps = 0;
     int maxd = 0;
     for (;;) {
         double P[27];
@@ -805,6 +819,7 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
             }
         } else {
             const int k = min(32, W.cnt[D]);
+            HV_CHECK(D > 0 && D < MAX_DEPTH && k > 0 && k <= top);
             act = lane < k;
             d = D;
             if (act) {
@@ -821,6 +836,7 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
         __syncwarp();
         const unsigned actmask = __ballot_sync(0xffffffffu, act);
         if (STATS && actmask) { nodes += __popc(actmask); maxd = max(maxd, d + 1); }
+        if (STATS) ++steps;
         // ---- split every active node into its 8 children --------------------
         double G1[45];
         split_xi(P, G1);
@@ -863,6 +879,7 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
                         const unsigned bm = hz ? b1 : b0;
                         if (bm & (1u << lane)) {
                             const int slot = top + pushed + (hz ? c0 : 0) + __popc(bm & lt_mask);
+                            HV_CHECK(slot >= 0 && slot < K4_CAP && owner >= 0 && owner < 32);
 #pragma unroll
                             for (int v = 0; v < 3; ++v)
 #pragma unroll
@@ -909,6 +926,7 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
             if (nsub) {
                 atomicAdd(&stats->n_subdivided, nsub);
                 atomicAdd(&stats->n_nodes, nodes);
+                atomicAdd(&stats->n_lane_steps, 32ull * steps);
                 atomicMax(&stats->max_depth, (unsigned long long)maxd);
                 if (n_inv) atomicAdd(&stats->n_invalid, n_inv);
                 if (n_val) atomicAdd(&stats->n_valid, n_val);
@@ -1047,6 +1065,7 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol
             }
         } else {
             const int k = min(32, W.cnt[D]);
+            HV_CHECK(D > 0 && D < MAX_DEPTH && k > 0 && k <= top);
             d = D;
             if (lane < k) {
                 const int slot = top - k + lane;
@@ -1117,6 +1136,7 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol
                         const unsigned bm = hz ? b1 : b0;
                         if (bm & (1u << lane)) {
                             const int slot = top + pushed + (hz ? c0 : 0) + __popc(bm & lt_mask);
+                            HV_CHECK(slot >= 0 && slot < K4_CAP && owner >= 0 && owner < 32);
 #pragma unroll
                             for (int v = 0; v < 3; ++v)
 #pragma unroll
@@ -1253,7 +1273,10 @@ __global__ void __launch_bounds__(SEL_THREADS) select_write_kernel(const uint8_t
     for (int q = 0; q < SEL_THREADS / 32; ++q) before += q < w ? s_w[q] : 0u;
     unsigned pos = tile_offsets[blockIdx.x] + before + x - c;
 #pragma unroll 1
-    for (unsigned r = m; r; r &= r - 1) ids[pos++] = (int32_t)(i0 + __ffs(r) - 1);
+    for (unsigned r = m; r; r &= r - 1) {
+        HV_CHECK((int64_t)pos < n);
+        ids[pos++] = (int32_t)(i0 + __ffs(r) - 1);
+    }
 }
 
 // ---------------------------------------------------------------------------

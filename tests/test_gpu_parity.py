@@ -599,3 +599,19 @@ def test_node_relabelling_by_cube_rotation_preserves_verdict():
     perm = [1, 2, 3, 0, 5, 6, 7, 4]
     f1, _ = gpu_soa(hexgen.nodes_to_soa(X[:, perm]))
     assert np.array_equal((f1 & 3)[sure], (f0 & 3)[sure])
+
+
+def test_debug_build_invariants(tmp_path):
+    """The HEXVAL_DEBUG build traps on any violated stack-capacity / index invariant
+    (compute-sanitizer is not available on the GPU pool): run every entry point on small
+    and adversarial inputs against it in a subprocess and require a clean exit."""
+    import subprocess
+    import sys
+    from paper_1706_01613_b200 import build as hvbuild
+    if not os.path.exists(hvbuild.DEBUG_LIB):
+        pytest.skip("libhexval_debug.so not built")
+    root = hexgen.__file__.rsplit("/", 2)[0]
+    env = dict(os.environ, HEXVAL_LIB="libhexval_debug.so")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_small.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
