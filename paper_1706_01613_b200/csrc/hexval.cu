@@ -485,21 +485,31 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
     if (STATS) cnt.flush(stats);
 }
 
-// K2 (cp.async variant): the same pipeline for int32 connectivity.  The 8
-// vertex ids of the thread's hex two tiles ahead are loaded into registers one
-// iteration early (their latency hides behind a whole tile of compute), then
-// the 24 coordinates are gathered into shared memory with async copies (L1
-// allocating: neighbouring hexes share vertices).
-__device__ __forceinline__ void load_idx8(const int32_t* __restrict__ idx, int64_t n, int64_t i, int4& a, int4& b) {
+// K2 (cp.async variant): the same pipeline for int32 connectivity, three deep:
+// while a thread computes its hex of tile k, the coordinates of its hex in
+// tile k+1 are in flight (gathered with async copies from the vertex array,
+// L1-allocating: neighbouring hexes share vertices) and so is the 32-byte
+// connectivity row of tile k+2 (two 16-byte async copies into shared memory);
+// after computing, the thread reads that row from shared memory and issues the
+// gathers of tile k+2.  No register holds prefetched data across the compute.
+constexpr size_t CPI_SMEM = CP_SMEM + (size_t)2 * CP_THREADS * 32;   // + two idx tiles
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_idx_row(const int32_t* __restrict__ idx, int64_t n, int64_t i, uint32_t dst) {
     if (i < n) {
-        a = __ldcs(reinterpret_cast<const int4*>(idx) + 2 * i);
-        b = __ldcs(reinterpret_cast<const int4*>(idx) + 2 * i + 1);
+        cp_async16(dst, idx + 8 * i);
+        cp_async16(dst + 16, idx + 8 * i + 4);
     }
 }
 
-__device__ __forceinline__ void cp_gather_hex(const double* __restrict__ verts, int64_t n, int64_t i, const int4& a,
-                                              const int4& b, uint32_t dst) {
+__device__ __forceinline__ void cp_gather_row(const double* __restrict__ verts, int64_t n, int64_t i,
+                                              const int32_t* row, uint32_t dst) {
     if (i < n) {
+        const int4 a = *reinterpret_cast<const int4*>(row);
+        const int4 b = *reinterpret_cast<const int4*>(row + 4);
         const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
         uint64_t policy;
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(policy));
@@ -510,7 +520,6 @@ __device__ __forceinline__ void cp_gather_hex(const double* __restrict__ verts, 
             for (int ax = 0; ax < 3; ++ax) cp_async8(dst + (3 * k + ax) * CP_THREADS * 8, src + ax, policy);
         }
     }
-    cp_async_commit();
 }
 
 template <bool COEFFS, bool STATS>
@@ -518,24 +527,32 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
     pass1_idx_cp_kernel(const double* __restrict__ verts, const int32_t* __restrict__ idx, int64_t n,
                         uint8_t* __restrict__ flags, double* __restrict__ coeffs, Ctl* ctl,
                         uint32_t* __restrict__ qsub, uint32_t* __restrict__ qexact, hexval_stats* stats) {
-    extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS]
+    extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS] coords, then [2][CP_THREADS][8] ids
     const int tid = threadIdx.x;
     const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
     const int64_t G = gridDim.x;
     const uint32_t s0 = smem_u32(cp_buf + tid);
     const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
+    int32_t* const rows = reinterpret_cast<int32_t*>(cp_buf + 2 * 24 * CP_THREADS);
+    int32_t* const row0 = rows + 8 * tid;                     // id row of tiles with even k
+    int32_t* const row1 = rows + 8 * (CP_THREADS + tid);      // ... odd k
+    const uint32_t r0 = smem_u32(row0), r1 = smem_u32(row1);
     const IdxLoader ld{verts, idx};
     P1Counts cnt;
     int64_t t = blockIdx.x;
-    int4 a, b;
-    load_idx8(idx, n, t * CP_THREADS + tid, a, b);
-    cp_gather_hex(verts, n, t * CP_THREADS + tid, a, b, s0);
-    load_idx8(idx, n, (t + G) * CP_THREADS + tid, a, b);
-    cp_gather_hex(verts, n, (t + G) * CP_THREADS + tid, a, b, s1);
-    load_idx8(idx, n, (t + 2 * G) * CP_THREADS + tid, a, b);
+    // prologue: rows of tiles 0 and 1 synchronously, then groups G0 = {gathers 0, row 2}, G1 = {gathers 1, row 3}
+    cp_idx_row(idx, n, t * CP_THREADS + tid, r0);
+    cp_idx_row(idx, n, (t + G) * CP_THREADS + tid, r1);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    cp_gather_row(verts, n, t * CP_THREADS + tid, row0, s0);
+    cp_idx_row(idx, n, (t + 2 * G) * CP_THREADS + tid, r0);
+    cp_async_commit();
+    cp_gather_row(verts, n, (t + G) * CP_THREADS + tid, row1, s1);
+    cp_idx_row(idx, n, (t + 3 * G) * CP_THREADS + tid, r1);
+    cp_async_commit();
     for (int k = 0; t < tiles; t += G, ++k) {
         const int bb = k & 1;
-        cp_async_wait1();
+        cp_async_wait1();                                    // group k: coords of tile k, row of tile k+2
         const int64_t i = t * CP_THREADS + tid;
         int st = -1;
         if (i < n) {
@@ -545,8 +562,10 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
             for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
             st = pass1_hex<COEFFS>(ld, X, i, n, flags, coeffs);
         }
-        cp_gather_hex(verts, n, (t + 2 * G) * CP_THREADS + tid, a, b, bb ? s1 : s0);
-        load_idx8(idx, n, (t + 3 * G) * CP_THREADS + tid, a, b);
+        // group k+2: gathers of tile k+2 (row read from shared memory), row of tile k+4
+        cp_gather_row(verts, n, (t + 2 * G) * CP_THREADS + tid, bb ? row1 : row0, bb ? s1 : s0);
+        cp_idx_row(idx, n, (t + 4 * G) * CP_THREADS + tid, bb ? r1 : r0);
+        cp_async_commit();
         warp_epilogue<false>(st, i, ctl, qsub, qexact, stats);
         if (STATS) cnt.add(st);
     }
@@ -651,9 +670,26 @@ constexpr int K4_WARPS = K4_THREADS / 32;
 constexpr int K4_CAP = (MAX_DEPTH - 1) * 256;
 
 struct WarpStacks {
-    double* coef;           // [warp][27][K4_CAP], node layout i + 3j + 9k
+    double* coef;           // [warp][14][K4_CAP] double2: coefficient pairs (2p, 2p+1) of layout i + 3j + 9k
     unsigned char* owner;   // [warp][K4_CAP], batch slot (lane) of the node's hex
 };
+
+// A node on the stack: 14 16-byte vectors per slot (the 28th value is padding),
+// so a push or a pop is 14 vector accesses, coalesced over the warp's slots.
+__device__ __forceinline__ void stack_load(const double* sc, int slot, double* P) {
+    const double2* s2 = reinterpret_cast<const double2*>(sc);
+#pragma unroll
+    for (int q = 0; q < 14; ++q) {
+        const double2 v = s2[(size_t)q * K4_CAP + slot];
+        P[2 * q] = v.x;
+        if (2 * q + 1 < 27) P[2 * q + 1] = v.y;
+    }
+}
+__device__ __forceinline__ void stack_store(double* sc, int slot, const double* C) {
+    double2* s2 = reinterpret_cast<double2*>(sc);
+#pragma unroll
+    for (int q = 0; q < 14; ++q) s2[(size_t)q * K4_CAP + slot] = make_double2(C[2 * q], 2 * q + 1 < 27 ? C[2 * q + 1] : 0.0);
+}
 
 // One line (p0, p1, p2) split at t = 1/2: m01 = (p0+p1)/2, m = (p0+2p1+p2)/4,
 // m12 = (p1+p2)/2 (A.4 of SURVEY.md; 1 DMUL + 4 DFMA).
@@ -752,7 +788,7 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
     const int lane = threadIdx.x & 31;
     K4Warp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
-    double* const sc = ws.coef + gw * 27 * K4_CAP;
+    double* const sc = ws.coef + gw * 28 * K4_CAP;
     unsigned char* const so = ws.owner + gw * K4_CAP;
     const unsigned total = *((volatile unsigned*)&ctl->n_sub);
     const unsigned n_exact = *((volatile unsigned*)&ctl->n_exact);
@@ -824,8 +860,7 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
             d = D;
             if (act) {
                 const int slot = top - k + lane;
-#pragma unroll
-                for (int c = 0; c < 27; ++c) P[c] = sc[(size_t)c * K4_CAP + slot];
+                stack_load(sc, slot, P);
                 owner = so[slot];
                 act = (W.status[owner] & 1u) == 0;       // hex already INVALID: drop the node
             }
@@ -880,13 +915,14 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
                         if (bm & (1u << lane)) {
                             const int slot = top + pushed + (hz ? c0 : 0) + __popc(bm & lt_mask);
                             HV_CHECK(slot >= 0 && slot < K4_CAP && owner >= 0 && owner < 32);
+                            double C[27];
 #pragma unroll
                             for (int v = 0; v < 3; ++v)
 #pragma unroll
                                 for (int u = 0; u < 3; ++u)
 #pragma unroll
-                                    for (int a = 0; a < 3; ++a)
-                                        sc[(size_t)(a + 3 * u + 9 * v) * K4_CAP + slot] = Z[a + 3 * u + 9 * (2 * hz + v)];
+                                    for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
+                            stack_store(sc, slot, C);
                             so[slot] = (unsigned char)owner;
                         }
                     }
@@ -1019,7 +1055,7 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol
     const int lane = threadIdx.x & 31;
     BWarp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
-    double* const sc = ws.coef + gw * 27 * K4_CAP;
+    double* const sc = ws.coef + gw * 28 * K4_CAP;
     unsigned char* const so = ws.owner + gw * K4_CAP;
     const unsigned lt_mask = (1u << lane) - 1u;
     if (lane <= MAX_DEPTH) W.cnt[lane] = 0;
@@ -1069,8 +1105,7 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol
             d = D;
             if (lane < k) {
                 const int slot = top - k + lane;
-#pragma unroll
-                for (int c = 0; c < 27; ++c) P[c] = sc[(size_t)c * K4_CAP + slot];
+                stack_load(sc, slot, P);
                 owner = so[slot];
                 // upper may have dropped since the push: the node may now be a leaf
                 double mn = P[0];
@@ -1137,13 +1172,14 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol
                         if (bm & (1u << lane)) {
                             const int slot = top + pushed + (hz ? c0 : 0) + __popc(bm & lt_mask);
                             HV_CHECK(slot >= 0 && slot < K4_CAP && owner >= 0 && owner < 32);
+                            double C[27];
 #pragma unroll
                             for (int v = 0; v < 3; ++v)
 #pragma unroll
                                 for (int u = 0; u < 3; ++u)
 #pragma unroll
-                                    for (int a = 0; a < 3; ++a)
-                                        sc[(size_t)(a + 3 * u + 9 * v) * K4_CAP + slot] = Z[a + 3 * u + 9 * (2 * hz + v)];
+                                    for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
+                            stack_store(sc, slot, C);
                             so[slot] = (unsigned char)owner;
                         }
                     }
@@ -1384,8 +1420,9 @@ int cp_setup() {
                           (const void*)pass1_soa_cp_kernel<true, false>, (const void*)pass1_soa_cp_kernel<true, true>,
                           (const void*)pass1_idx_cp_kernel<false, false>, (const void*)pass1_idx_cp_kernel<false, true>,
                           (const void*)pass1_idx_cp_kernel<true, false>, (const void*)pass1_idx_cp_kernel<true, true>};
-    for (const void* f : fns)
-        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CP_SMEM) != cudaSuccess) {
+    for (int f = 0; f < 8; ++f)
+        if (cudaFuncSetAttribute(fns[f], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(f < 4 ? CP_SMEM : CPI_SMEM)) !=
+            cudaSuccess) {
             cudaGetLastError();
             return 0;
         }
@@ -1484,11 +1521,11 @@ void launch_pass1<IdxLoader>(const IdxLoader& ld, const DeviceInfo& info, int64_
     const double* v = ld.verts;
     const int32_t* x = ld.idx;
     if (coeffs) {
-        if (stats) pass1_idx_cp_kernel<true, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_idx_cp_kernel<true, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+        if (stats) pass1_idx_cp_kernel<true, true><<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_idx_cp_kernel<true, false><<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
     } else {
-        if (stats) pass1_idx_cp_kernel<false, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_idx_cp_kernel<false, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+        if (stats) pass1_idx_cp_kernel<false, true><<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+        else pass1_idx_cp_kernel<false, false><<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
     }
 }
 
@@ -1572,7 +1609,7 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     if (prof && prof->count >= hexval_profile::CAP) return HEXVAL_ERR_ARGUMENT;   // read it first
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
-    const size_t sc_bytes = warps * 27 * K4_CAP * sizeof(double);
+    const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
     const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
     const size_t total = ctl_bytes + 2 * q_bytes + sc_bytes + so_bytes;
     char* base = nullptr;
@@ -1647,7 +1684,7 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     const size_t warps = (size_t)info.sms * info.k4_blocks_per_sm * K4_WARPS;
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
-    const size_t sc_bytes = warps * 27 * K4_CAP * sizeof(double);
+    const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
     const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
     char* base = nullptr;
     if (cudaMallocAsync((void**)&base, ctl_bytes + q_bytes + sc_bytes + so_bytes, stream) != cudaSuccess) {
@@ -1684,7 +1721,7 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     const int64_t blocks = (int64_t)info.sms * occ;
     const size_t warps = (size_t)blocks * K4_WARPS;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
-    const size_t sc_bytes = warps * 27 * K4_CAP * sizeof(double);
+    const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
     const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
     char* base = nullptr;
     if (cudaMallocAsync((void**)&base, 256 + q_bytes + sc_bytes + so_bytes, stream) != cudaSuccess) {

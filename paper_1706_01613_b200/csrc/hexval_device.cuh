@@ -163,12 +163,21 @@ __device__ __forceinline__ void transform(const Samples& s, Coeffs& t) {
     t.e2[11] = __dsub_rn(__dsub_rn(d[11], c[4]), c[7]);
     // faces 21..26: corners {1234} {1256} {2367} {3478} {1458} {5678}
     //               edges   {9,10,11,12} {9,13,14,17} {10,14,15,18} {11,15,16,19} {12,13,16,20} {17,18,19,20}
-    const double D21 = sum4(d[0], d[1], d[2], d[3]), C21 = sum4(c[0], c[1], c[2], c[3]);
-    const double D22 = sum4(d[0], d[4], d[5], d[8]), C22 = sum4(c[0], c[1], c[4], c[5]);
-    const double D23 = sum4(d[1], d[5], d[6], d[9]), C23 = sum4(c[1], c[2], c[5], c[6]);
-    const double D24 = sum4(d[2], d[6], d[7], d[10]), C24 = sum4(c[2], c[3], c[6], c[7]);
-    const double D25 = sum4(d[3], d[4], d[7], d[11]), C25 = sum4(c[0], c[3], c[4], c[7]);
-    const double D26 = sum4(d[8], d[9], d[10], d[11]), C26 = sum4(c[4], c[5], c[6], c[7]);
+    // Corner sums through shared pairs (14 adds instead of 18); the 4 vertical
+    // edge pairs of faces 22 and 24 are reused by the centre row.
+    const double p01 = __dadd_rn(c[0], c[1]), p23 = __dadd_rn(c[2], c[3]);
+    const double p45 = __dadd_rn(c[4], c[5]), p67 = __dadd_rn(c[6], c[7]);
+    const double C21 = __dadd_rn(p01, p23), C26 = __dadd_rn(p45, p67);
+    const double C22 = __dadd_rn(p01, p45), C24 = __dadd_rn(p23, p67);
+    const double C23 = __dadd_rn(__dadd_rn(c[1], c[2]), __dadd_rn(c[5], c[6]));
+    const double C25 = __dadd_rn(__dadd_rn(c[0], c[3]), __dadd_rn(c[4], c[7]));
+    const double s45 = __dadd_rn(d[4], d[5]), s67 = __dadd_rn(d[6], d[7]);   // edges 13+14, 15+16
+    const double D21 = sum4(d[0], d[1], d[2], d[3]);
+    const double D26 = sum4(d[8], d[9], d[10], d[11]);
+    const double D22 = __dadd_rn(__dadd_rn(d[0], d[8]), s45);
+    const double D24 = __dadd_rn(__dadd_rn(d[2], d[10]), s67);
+    const double D23 = __dadd_rn(__dadd_rn(d[1], d[9]), __dadd_rn(d[5], d[6]));
+    const double D25 = __dadd_rn(__dadd_rn(d[3], d[11]), __dadd_rn(d[4], d[7]));
     t.f4[0] = __fma_rn(-3.0, C21, D21);
     t.f4[1] = __fma_rn(-3.0, C22, D22);
     t.f4[2] = __fma_rn(-3.0, C23, D23);
@@ -176,7 +185,7 @@ __device__ __forceinline__ void transform(const Samples& s, Coeffs& t) {
     t.f4[4] = __fma_rn(-3.0, C25, D25);
     t.f4[5] = __fma_rn(-3.0, C26, D26);
     // centre: all 12 edges = bottom ring + top ring + 4 verticals; all 8 corners
-    const double Dall = __dadd_rn(__dadd_rn(D21, D26), sum4(d[4], d[5], d[6], d[7]));
+    const double Dall = __dadd_rn(__dadd_rn(D21, D26), __dadd_rn(s45, s67));
     const double Call = __dadd_rn(C21, C26);
     t.z8 = __fma_rn(-5.0, Call, Dall);
 }
