@@ -670,25 +670,30 @@ constexpr int K4_WARPS = K4_THREADS / 32;
 constexpr int K4_CAP = (MAX_DEPTH - 1) * 256;
 
 struct WarpStacks {
-    double* coef;           // [warp][14][K4_CAP] double2: coefficient pairs (2p, 2p+1) of layout i + 3j + 9k
-    unsigned char* owner;   // [warp][K4_CAP], batch slot (lane) of the node's hex
+    double* coef;           // [warp][14][K4_CAP] double2: coefficient pairs (2p, 2p+1) of layout i + 3j + 9k,
+                            // the last pair's second half holding the owner (batch slot of the node's hex)
 };
 
-// A node on the stack: 14 16-byte vectors per slot (the 28th value is padding),
-// so a push or a pop is 14 vector accesses, coalesced over the warp's slots.
-__device__ __forceinline__ void stack_load(const double* sc, int slot, double* P) {
+// A node on the stack: 14 16-byte vectors per slot, the 28th value carrying
+// the node's owner (batch slot of its hex), so a push or a pop is 14 vector
+// accesses, coalesced over the warp's slots.
+__device__ __forceinline__ int stack_load(const double* sc, int slot, double* P) {
     const double2* s2 = reinterpret_cast<const double2*>(sc);
+    int owner = 0;
 #pragma unroll
     for (int q = 0; q < 14; ++q) {
         const double2 v = s2[(size_t)q * K4_CAP + slot];
         P[2 * q] = v.x;
         if (2 * q + 1 < 27) P[2 * q + 1] = v.y;
+        else owner = __double2loint(v.y);
     }
+    return owner;
 }
-__device__ __forceinline__ void stack_store(double* sc, int slot, const double* C) {
+__device__ __forceinline__ void stack_store(double* sc, int slot, const double* C, int owner) {
     double2* s2 = reinterpret_cast<double2*>(sc);
 #pragma unroll
-    for (int q = 0; q < 14; ++q) s2[(size_t)q * K4_CAP + slot] = make_double2(C[2 * q], 2 * q + 1 < 27 ? C[2 * q + 1] : 0.0);
+    for (int q = 0; q < 14; ++q)
+        s2[(size_t)q * K4_CAP + slot] = make_double2(C[2 * q], 2 * q + 1 < 27 ? C[2 * q + 1] : __hiloint2double(0, owner));
 }
 
 // One line (p0, p1, p2) split at t = 1/2: m01 = (p0+p1)/2, m = (p0+2p1+p2)/4,
@@ -789,7 +794,6 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
     K4Warp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
     double* const sc = ws.coef + gw * 28 * K4_CAP;
-    unsigned char* const so = ws.owner + gw * K4_CAP;
     const unsigned total = *((volatile unsigned*)&ctl->n_sub);
     const unsigned n_exact = *((volatile unsigned*)&ctl->n_exact);
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -860,8 +864,7 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
             d = D;
             if (act) {
                 const int slot = top - k + lane;
-                stack_load(sc, slot, P);
-                owner = so[slot];
+                owner = stack_load(sc, slot, P);
                 act = (W.status[owner] & 1u) == 0;       // hex already INVALID: drop the node
             }
             top -= k;
@@ -922,8 +925,8 @@ __global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_
                                 for (int u = 0; u < 3; ++u)
 #pragma unroll
                                     for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
-                            stack_store(sc, slot, C);
-                            so[slot] = (unsigned char)owner;
+                            stack_store(sc, slot, C, owner);
+
                         }
                     }
                     pushed += c0 + __popc(b1);
@@ -1056,7 +1059,6 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol
     BWarp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
     double* const sc = ws.coef + gw * 28 * K4_CAP;
-    unsigned char* const so = ws.owner + gw * K4_CAP;
     const unsigned lt_mask = (1u << lane) - 1u;
     if (lane <= MAX_DEPTH) W.cnt[lane] = 0;
     __syncwarp();
@@ -1105,8 +1107,7 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol
             d = D;
             if (lane < k) {
                 const int slot = top - k + lane;
-                stack_load(sc, slot, P);
-                owner = so[slot];
+                owner = stack_load(sc, slot, P);
                 // upper may have dropped since the push: the node may now be a leaf
                 double mn = P[0];
 #pragma unroll
@@ -1179,8 +1180,8 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol
                                 for (int u = 0; u < 3; ++u)
 #pragma unroll
                                     for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
-                            stack_store(sc, slot, C);
-                            so[slot] = (unsigned char)owner;
+                            stack_store(sc, slot, C, owner);
+
                         }
                     }
                     pushed += c0 + __popc(b1);
@@ -1610,8 +1611,7 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
-    const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
-    const size_t total = ctl_bytes + 2 * q_bytes + sc_bytes + so_bytes;
+    const size_t total = ctl_bytes + 2 * q_bytes + sc_bytes;
     char* base = nullptr;
     if (cudaMallocAsync((void**)&base, total, stream) != cudaSuccess) {
         cudaGetLastError();
@@ -1622,7 +1622,6 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     uint32_t* qex = reinterpret_cast<uint32_t*>(base + ctl_bytes + q_bytes);
     WarpStacks fr;
     fr.coef = reinterpret_cast<double*>(base + ctl_bytes + 2 * q_bytes);
-    fr.owner = reinterpret_cast<unsigned char*>(base + ctl_bytes + 2 * q_bytes + sc_bytes);
     cudaMemsetAsync(ctl, 0, ctl_bytes, stream);
 
     const int slot = prof ? prof->count++ : -1;
@@ -1685,9 +1684,8 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
-    const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
     char* base = nullptr;
-    if (cudaMallocAsync((void**)&base, ctl_bytes + q_bytes + sc_bytes + so_bytes, stream) != cudaSuccess) {
+    if (cudaMallocAsync((void**)&base, ctl_bytes + q_bytes + sc_bytes, stream) != cudaSuccess) {
         cudaGetLastError();
         return HEXVAL_ERR_ALLOC;
     }
@@ -1695,7 +1693,6 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     uint32_t* qsub = reinterpret_cast<uint32_t*>(base + ctl_bytes);
     WarpStacks fr;
     fr.coef = reinterpret_cast<double*>(base + ctl_bytes + q_bytes);
-    fr.owner = reinterpret_cast<unsigned char*>(base + ctl_bytes + q_bytes + sc_bytes);
     cudaMemsetAsync(ctl, 0, ctl_bytes, stream);
     const unsigned p1_blocks = (unsigned)((n + P1_THREADS - 1) / P1_THREADS);
     if (stats) bezier_pass_kernel<true><<<p1_blocks, P1_THREADS, 0, stream>>>(b, n, flags, ctl, qsub, stats);
@@ -1722,9 +1719,8 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     const size_t warps = (size_t)blocks * K4_WARPS;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
-    const size_t so_bytes = (warps * K4_CAP + 255) & ~(size_t)255;
     char* base = nullptr;
-    if (cudaMallocAsync((void**)&base, 256 + q_bytes + sc_bytes + so_bytes, stream) != cudaSuccess) {
+    if (cudaMallocAsync((void**)&base, 256 + q_bytes + sc_bytes, stream) != cudaSuccess) {
         cudaGetLastError();
         return HEXVAL_ERR_ALLOC;
     }
@@ -1732,7 +1728,6 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     uint32_t* q = reinterpret_cast<uint32_t*>(base + 256);
     WarpStacks ws;
     ws.coef = reinterpret_cast<double*>(base + 256 + q_bytes);
-    ws.owner = reinterpret_cast<unsigned char*>(base + 256 + q_bytes + sc_bytes);
     cudaMemsetAsync(ctlq, 0, 256, stream);
     bounds_root_kernel<L><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(ld, n, rel_tol, lower, upper, status, ctlq, q);
     bounds_kernel<L><<<(unsigned)blocks, K4_THREADS, 0, stream>>>(ld, rel_tol, lower, upper, status, ctlq, q, ws,
