@@ -45,7 +45,23 @@ using namespace hexval;
 namespace {
 
 constexpr int P1_THREADS = 256;
-constexpr int K4_THREADS = 128;
+// K4 / bounds kernel geometry (compile-time; A/B builds override with -D):
+// threads per block and the minimum number of resident blocks per SM that
+// bounds the register budget (128 x 2: <= 255 registers, 8 warps/SM).
+#ifndef HEXVAL_K4_THREADS
+#define HEXVAL_K4_THREADS 128
+#endif
+#ifndef HEXVAL_K4_MINB
+#define HEXVAL_K4_MINB 2
+#endif
+constexpr int K4_THREADS = HEXVAL_K4_THREADS;
+constexpr int K4_MINB = HEXVAL_K4_MINB;
+// optional explicit register cap (e.g. 1-warp blocks with -DHEXVAL_K4_MAXNREG=224: 9 warps/SM)
+#ifdef HEXVAL_K4_MAXNREG
+#define HV_K4_BOUNDS __maxnreg__(HEXVAL_K4_MAXNREG)
+#else
+#define HV_K4_BOUNDS __launch_bounds__(K4_THREADS, K4_MINB)
+#endif
 
 // flags placeholders written by pass 1 for hexes that later kernels finish
 constexpr uint8_t PENDING_EXACT = 0xFF;
@@ -755,6 +771,13 @@ struct K4Warp {
 // the pass-1 arithmetic (bit-identical), or read from caller-supplied Bezier
 // coefficients (hexval_classify_bezier).
 template <class L>
+__device__ __noinline__ uint8_t exact_hex(const L ld, uint32_t h) {
+    double X[24];
+    ld.load(h, X);
+    return face_pair_coincident(X) ? (uint8_t)HEXVAL_INVALID : exact_resolve(X);
+}
+
+template <class L>
 struct CoordRoot {
     L ld;
     __device__ __forceinline__ void operator()(uint32_t h, double* P) const {
@@ -766,12 +789,8 @@ struct CoordRoot {
         transform(s, t);
         root_coeffs(s, t, P);
     }
-    // K5 fused into K4: Steps 2-4 of an ambiguous hex with exact signs
-    __device__ __forceinline__ uint8_t exact(uint32_t h) const {
-        double X[24];
-        ld.load(h, X);
-        return face_pair_coincident(X) ? (uint8_t)HEXVAL_INVALID : exact_resolve(X);
-    }
+    // K5 fused into K4: Steps 2-4 of an ambiguous hex with exact signs (out of line)
+    __device__ __forceinline__ uint8_t exact(uint32_t h) const { return exact_hex(ld, h); }
 };
 
 struct CoeffRoot {
@@ -784,8 +803,8 @@ struct CoeffRoot {
     __device__ __forceinline__ uint8_t exact(uint32_t) const { return HEXVAL_FLAG_SUBDIVIDED; }   // no exact queue
 };
 
-template <class R, bool STATS, int MINB>
-__global__ void __launch_bounds__(K4_THREADS, MINB) subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
+template <class R, bool STATS>
+__global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
                                                             const uint32_t* __restrict__ qsub,
                                                             const uint32_t* __restrict__ qexact, WarpStacks ws,
                                                             hexval_stats* stats) {
@@ -1050,7 +1069,7 @@ __global__ void __launch_bounds__(256) bounds_root_kernel(L ld, int64_t n, doubl
 }
 
 template <class L>
-__global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol, double* __restrict__ lower_out,
+__global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restrict__ lower_out,
                                                             double* __restrict__ upper_out, uint8_t* __restrict__ status_out,
                                                             unsigned* ctlq, const uint32_t* __restrict__ q, WarpStacks ws,
                                                             unsigned long long* nodes_out) {
@@ -1133,23 +1152,18 @@ __global__ void __launch_bounds__(K4_THREADS) bounds_kernel(L ld, double rel_tol
             for (int hy = 0; hy < 2; ++hy) {
                 double Z[45];
                 split_quarter(G1, hx, hy, Z);
-                double cmin[2], amin[2];
+                // mins per zeta plane (the two children share plane 2): 5 plane
+                // mins and 3 plane-corner mins instead of two 27- and 8-value scans
+                double pm[5], pc[3];
 #pragma unroll
-                for (int hz = 0; hz < 2; ++hz) {
-                    double mc = Z[9 * 2 * hz], ma = Z[9 * 2 * hz];
-#pragma unroll
-                    for (int v = 0; v < 3; ++v)
-#pragma unroll
-                        for (int u = 0; u < 3; ++u)
-#pragma unroll
-                            for (int a = 0; a < 3; ++a) {
-                                const double z = Z[a + 3 * u + 9 * (2 * hz + v)];
-                                ma = dmin(ma, z);
-                                if (a != 1 && u != 1 && v != 1) mc = dmin(mc, z);
-                            }
-                    cmin[hz] = mc;
-                    amin[hz] = ma;
+                for (int v = 0; v < 5; ++v) {
+                    const double* z = Z + 9 * v;
+                    const double c4 = dmin(dmin(z[0], z[2]), dmin(z[6], z[8]));
+                    if (!(v & 1)) pc[v >> 1] = c4;
+                    pm[v] = dmin(dmin(dmin(c4, z[4]), dmin(z[1], z[3])), dmin(z[5], z[7]));
                 }
+                const double cmin[2] = {dmin(pc[0], pc[1]), dmin(pc[1], pc[2])};
+                const double amin[2] = {dmin(dmin(pm[0], pm[1]), pm[2]), dmin(dmin(pm[2], pm[3]), pm[4])};
                 if (act) atomicMin(&W.upper[owner], okey(dmin(cmin[0], cmin[1])));
                 __syncwarp();
                 const double U = okey_inv(W.upper[owner]);
@@ -1336,50 +1350,65 @@ __device__ __noinline__ int exact_orient2d(double ax, double ay, double bx, doub
     return kulisch_sign(acc);
 }
 
-__global__ void __launch_bounds__(256) quad_kernel(const double* __restrict__ coords, int64_t n,
-                                                    uint8_t* __restrict__ flags, double* __restrict__ J_out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double q[8];
-#pragma unroll
-    for (int p = 0; p < 8; ++p) q[p] = __ldcs(coords + (int64_t)p * n + i);
+__device__ __forceinline__ uint8_t quad_one(const double* q, double* J) {
     bool bad = false;
 #pragma unroll
     for (int p = 0; p < 8; ++p) bad |= !(fabs(q[p]) <= 0x1p300);
-    uint8_t f;
-    double J[4];
     if (bad) {
-        f = HEXVAL_NONFINITE;
 #pragma unroll
         for (int k = 0; k < 4; ++k) J[k] = __longlong_as_double(0x7ff8000000000000ll);
-    } else {
-        const double v12x = __dsub_rn(q[2], q[0]), v12y = __dsub_rn(q[3], q[1]);
-        const double v43x = __dsub_rn(q[4], q[6]), v43y = __dsub_rn(q[5], q[7]);
-        const double v14x = __dsub_rn(q[6], q[0]), v14y = __dsub_rn(q[7], q[1]);
-        const double v23x = __dsub_rn(q[4], q[2]), v23y = __dsub_rn(q[5], q[3]);
-        // corner k: J_k = u x w (reading Q1: J3 at (1,1) pairs v43 with v23)
-        const double ux[4] = {v12x, v12x, v43x, v43x}, uy[4] = {v12y, v12y, v43y, v43y};
-        const double wx[4] = {v14x, v23x, v23x, v14x}, wy[4] = {v14y, v23y, v23y, v14y};
-        // (origin, xi-neighbour, eta-neighbour) of each corner as an orientation of input points
-        const int o[4][3] = {{0, 1, 3}, {0, 1, 2}, {2, 3, 1}, {3, 0, 2}};
-        bool valid = true;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const double a = __dmul_rn(ux[k], wy[k]), b = __dmul_rn(uy[k], wx[k]);
-            J[k] = __dsub_rn(a, b);
-            // |fl(J) - J| <= 8 u (|a| + |b|) for inputs with rounded differences (+ underflow)
-            const double tau = __fma_rn(8.0 * U_ROUND, __dadd_rn(fabs(a), fabs(b)), 0x1p-1060);
-            if (J[k] < -tau) valid = false;
-            else if (!(J[k] > tau) && valid)
-                valid = exact_orient2d(q[2 * o[k][0]], q[2 * o[k][0] + 1], q[2 * o[k][1]], q[2 * o[k][1] + 1],
-                                       q[2 * o[k][2]], q[2 * o[k][2] + 1]) > 0;
-        }
-        f = valid ? HEXVAL_VALID : HEXVAL_INVALID;
+        return HEXVAL_NONFINITE;
     }
-    __stcs(flags + i, f);
-    if (J_out)
+    const double v12x = __dsub_rn(q[2], q[0]), v12y = __dsub_rn(q[3], q[1]);
+    const double v43x = __dsub_rn(q[4], q[6]), v43y = __dsub_rn(q[5], q[7]);
+    const double v14x = __dsub_rn(q[6], q[0]), v14y = __dsub_rn(q[7], q[1]);
+    const double v23x = __dsub_rn(q[4], q[2]), v23y = __dsub_rn(q[5], q[3]);
+    // corner k: J_k = u x w (reading Q1: J3 at (1,1) pairs v43 with v23)
+    const double ux[4] = {v12x, v12x, v43x, v43x}, uy[4] = {v12y, v12y, v43y, v43y};
+    const double wx[4] = {v14x, v23x, v23x, v14x}, wy[4] = {v14y, v23y, v23y, v14y};
+    // (origin, xi-neighbour, eta-neighbour) of each corner as an orientation of input points
+    const int o[4][3] = {{0, 1, 3}, {0, 1, 2}, {2, 3, 1}, {3, 0, 2}};
+    bool valid = true;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) __stcs(J_out + (int64_t)k * n + i, J[k]);
+    for (int k = 0; k < 4; ++k) {
+        const double a = __dmul_rn(ux[k], wy[k]), b = __dmul_rn(uy[k], wx[k]);
+        J[k] = __dsub_rn(a, b);
+        // |fl(J) - J| <= 8 u (|a| + |b|) for inputs with rounded differences (+ underflow)
+        const double tau = __fma_rn(8.0 * U_ROUND, __dadd_rn(fabs(a), fabs(b)), 0x1p-1060);
+        if (J[k] < -tau) valid = false;
+        else if (!(J[k] > tau) && valid)
+            valid = exact_orient2d(q[2 * o[k][0]], q[2 * o[k][0] + 1], q[2 * o[k][1]], q[2 * o[k][1] + 1],
+                                   q[2 * o[k][2]], q[2 * o[k][2] + 1]) > 0;
+    }
+    return valid ? HEXVAL_VALID : HEXVAL_INVALID;
+}
+
+// QPT quads per thread, their 8*QPT loads issued before any compute (bytes in
+// flight: the kernel is HBM bound at 65 B/quad with ~30 FP64 ops)
+constexpr int QPT = 4;
+
+__global__ void __launch_bounds__(256) quad_kernel(const double* __restrict__ coords, int64_t n,
+                                                    uint8_t* __restrict__ flags, double* __restrict__ J_out) {
+    const int64_t i0 = (int64_t)blockIdx.x * (256 * QPT) + threadIdx.x;
+    double q[QPT][8];
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+        const int64_t i = i0 + j * 256;
+        if (i < n)
+#pragma unroll
+            for (int p = 0; p < 8; ++p) q[j][p] = __ldcs(coords + (int64_t)p * n + i);
+    }
+#pragma unroll
+    for (int j = 0; j < QPT; ++j) {
+        const int64_t i = i0 + j * 256;
+        if (i >= n) break;
+        double J[4];
+        const uint8_t f = quad_one(q[j], J);
+        __stcs(flags + i, f);
+        if (J_out)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) __stcs(J_out + (int64_t)k * n + i, J[k]);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1388,7 +1417,6 @@ __global__ void __launch_bounds__(256) quad_kernel(const double* __restrict__ co
 struct DeviceInfo {
     int sms = 0;
     int k4_blocks_per_sm = 0;
-    int k4_minb = 2;
     int p1_variant = 0;           // SoA pass 1: P1_LDG (plain), P1_WTMA or P1_CP
     int p1_ctas_per_sm = 1;
     bool ok = false;
@@ -1454,14 +1482,7 @@ const DeviceInfo& device_info(int dev) {
     if (!d.ok) {
         cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        // K4 register budget: HEXVAL_K4_MINB = 2 (<= 255 regs, 8 warps/SM, no spills) or 3 (<= 168 regs,
-        // 12 warps/SM, small spills) -- tuning knob for measurements
-        const char* mb = getenv("HEXVAL_K4_MINB");
-        d.k4_minb = (mb && atoi(mb) == 3) ? 3 : 2;
-        if (d.k4_minb == 3)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false, 3>, K4_THREADS, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false, 2>, K4_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false>, K4_THREADS, 0);
         d.k4_blocks_per_sm = occ > 0 ? occ : 1;
         const int want = pass1_variant_from_env();
         const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup() : 0);
@@ -1576,13 +1597,8 @@ template <class R>
 void launch_subdiv(const R& root, const DeviceInfo& info, unsigned blocks, uint8_t* flags, Ctl* ctl,
                    const uint32_t* qsub, const uint32_t* qex, const WarpStacks& fr, hexval_stats* stats,
                    cudaStream_t stream) {
-    if (info.k4_minb == 3) {
-        if (stats) subdiv_kernel<R, true, 3><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
-        else subdiv_kernel<R, false, 3><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
-    } else {
-        if (stats) subdiv_kernel<R, true, 2><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
-        else subdiv_kernel<R, false, 2><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
-    }
+    if (stats) subdiv_kernel<R, true><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
+    else subdiv_kernel<R, false><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
 }
 
 int collect_profile(hexval_profile* p) {
@@ -1847,7 +1863,7 @@ int hexval_check_quad_soa(const double* coords, int64_t n, uint8_t* flags_out, d
     if (n > 0 && (!coords || !flags_out)) return HEXVAL_ERR_ARGUMENT;
     if (misaligned(coords, 8) || misaligned(J_out_opt, 8)) return HEXVAL_ERR_ALIGNMENT;
     if (n == 0) return HEXVAL_OK;
-    quad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(coords, n, flags_out, J_out_opt);
+    quad_kernel<<<(unsigned)((n + 256 * QPT - 1) / (256 * QPT)), 256, 0, stream>>>(coords, n, flags_out, J_out_opt);
     return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
 }
 
