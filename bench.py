@@ -67,6 +67,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
+    p.add_argument("--coeffs", action="store_true",
+                   help="also write the 27 Bezier coefficients per hex (409 B/hex, SURVEY.md 8(d))")
     p.add_argument("--op", choices=["check", "quality", "bounds", "select", "quads"], default="check",
                    help="check: the hot path (headline); quality: NEXT-2 corner screening kernel; "
                         "bounds: NEXT-1 certified min det J bounds; select: NEXT-3 candidate filtering "
@@ -180,17 +182,17 @@ def barrier(world: int):
 # ---------------------------------------------------------------------------
 # CPU oracle (baseline / reference arm)
 # ---------------------------------------------------------------------------
-def oracle_sample(cfg: int, m: int, start: int = 0):
+def oracle_sample(cfg: int, m: int, start: int = 0, nthreads: int = 0):
     import hexgen
     import oracle
     if cfg in (0, 1):
         coords = hexgen.soa_config(m, 0.25 if cfg == 0 else 0.35, cfg, start)
-        return lambda: oracle.check_soa(coords)
+        return lambda: oracle.check_soa(coords, nthreads=nthreads)
     if cfg == 4:
         coords, _ = hexgen.adversarial_config(m, 4, start)
-        return lambda: oracle.check_soa(coords)
+        return lambda: oracle.check_soa(coords, nthreads=nthreads)
     _, verts, idx = hexgen.make(cfg, start, m)
-    return lambda: oracle.check_indexed(verts, idx)
+    return lambda: oracle.check_indexed(verts, idx, nthreads=nthreads)
 
 
 def oracle_rate(cfg: int, seconds: float, start: int = 0):
@@ -210,8 +212,16 @@ def oracle_rate(cfg: int, seconds: float, start: int = 0):
     t0 = time.perf_counter()
     run()
     dt = time.perf_counter() - t0
+    # one thread on a smaller slice of the same stream (per-core rate, the unit of the
+    # paper's ~6 M hex/s on one core)
+    m1 = max(1000, min(m, int(m / max(1, cores) / 4)))
+    run1 = oracle_sample(cfg, m1, start, nthreads=1)
+    t1 = time.perf_counter()
+    run1()
+    dt1 = time.perf_counter() - t1
     return {"value": m / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"hexes {start}..{start + m - 1} of {CONFIG_DESC[cfg]} ({m} hexes, {dt:.2f} s wall on {cores} threads)"}
+            "sample": f"hexes {start}..{start + m - 1} of {CONFIG_DESC[cfg]} ({m} hexes, {dt:.2f} s wall on {cores} threads)",
+            "single_thread": {"value": m1 / dt1, "unit": UNIT, "sample": f"hexes {start}..{start + m1 - 1}, 1 thread"}}
 
 
 def run_reference(args, world, rank):
@@ -260,12 +270,14 @@ def make_inputs(cfg: int, rank: int):
     return "indexed", n, (verts, idx)
 
 
-def algorithmic_bytes(layout: str, n: int, arrays) -> int:
-    """Compulsory HBM bytes of one pass-1 launch: inputs once + 1 flag byte/hex."""
+def algorithmic_bytes(layout: str, n: int, arrays, coeffs: bool = False) -> int:
+    """Compulsory HBM bytes of one pass-1 launch: inputs once + 1 flag byte/hex
+    (+ 27 fp64 coefficients per hex when they are written)."""
+    out = n + (216 * n if coeffs else 0)
     if layout == "soa":
-        return 193 * n
+        return 192 * n + out
     verts, idx = arrays
-    return 32 * n + 24 * verts.shape[0] + n
+    return 32 * n + 24 * verts.shape[0] + out
 
 
 def run_ours(args, world, rank, local):
@@ -279,13 +291,14 @@ def run_ours(args, world, rank, local):
     layout, n, host = make_inputs(cfg, rank)
     dev = [torch.from_numpy(a).cuda() for a in host]
     flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    coeffs = torch.empty((27, n), dtype=torch.float64, device="cuda") if args.coeffs else None
     stream = torch.cuda.current_stream()
 
     def step(profile=None, stats=None):
         if layout == "soa":
-            hv.check_soa(dev[0], flags=flags, profile=profile, stats=stats)
+            hv.check_soa(dev[0], flags=flags, coeffs=coeffs, profile=profile, stats=stats)
         else:
-            hv.check_indexed(dev[0], dev[1], flags=flags, profile=profile, stats=stats)
+            hv.check_indexed(dev[0], dev[1], flags=flags, coeffs=coeffs, profile=profile, stats=stats)
 
     # untimed: verdict / subdivision statistics of this workload
     stats = hv.Stats()
@@ -323,7 +336,7 @@ def run_ours(args, world, rank, local):
 
     value = world * n / (ms_step * 1e-3)
     peak, peak_src = measured_peaks()
-    algo = algorithmic_bytes(layout, n, host)
+    algo = algorithmic_bytes(layout, n, host, args.coeffs)
     achieved = algo / (pass1_ms * 1e-3) / 1e9
     traffic = ncu_traffic()
     roofline = {
@@ -331,8 +344,8 @@ def run_ours(args, world, rank, local):
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "peak_source": peak_src,
         "algorithmic_bytes_per_launch": algo,
-        "traffic": (traffic["dram_bytes_per_hex"] * n if traffic and cfg == 1 else None),
-        "traffic_source": (traffic.get("source") if traffic and cfg == 1 else None),
+        "traffic": (traffic["dram_bytes_per_hex"] * n if traffic and cfg == 1 and not args.coeffs else None),
+        "traffic_source": (traffic.get("source") if traffic and cfg == 1 and not args.coeffs else None),
         "frac_of_8TBs_nominal": achieved / 8000.0,
         "pass1_ms": pass1_ms,
         "pass1_share_of_step": pass1_ms / ms_step,
@@ -393,7 +406,8 @@ def run_ours(args, world, rank, local):
             "config": {"workload": desc, "n_hexes_per_rank": n, "global_hexes": world * n, "layout": layout,
                        "parallelism": f"independent shards x{world}" if world > 1 else "single GPU",
                        "l2": L2_NOTE[cfg],
-                       "pass1_variant": os.environ.get("HEXVAL_PASS1", "default")},
+                       "pass1_variant": os.environ.get("HEXVAL_PASS1", "default"),
+                       "coefficients_written": bool(args.coeffs)},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
