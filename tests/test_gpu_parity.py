@@ -615,3 +615,39 @@ def test_debug_build_invariants(tmp_path):
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_small.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
+
+
+# --------------------------------------------------------------------------
+# large sizes: 64-bit plane offsets (p * n * 8 > 2^32) and long queues
+# --------------------------------------------------------------------------
+
+def test_large_soa_input_sampled():
+    """n = 2^28 + 3 hexes (51.5 GB of coordinates): plane offsets exceed 32 bits, the
+    persistent kernels run ~3600 tiles per CTA; generated on the device from a seeded
+    torch generator (perturbed unit cubes, amplitude 0.45), checked on a sample that
+    includes the last hexes of the array."""
+    n = (1 << 28) + 3
+    free, _ = torch.cuda.mem_get_info()
+    if free < 60e9:
+        pytest.skip("needs ~60 GB of free device memory")
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    coords = torch.rand((24, n), generator=g, device="cuda", dtype=torch.float64).mul_(0.9).sub_(0.45)
+    cube = torch.from_numpy(pins.KAPPA.astype(np.float64).reshape(24, 1)).cuda()
+    coords.add_(cube)
+    stats = hv.Stats()
+    f, _ = hv.check_soa(coords, stats=stats)
+    torch.cuda.synchronize()
+    st = stats.read()
+    assert st["n_valid"] + st["n_invalid"] + st["n_undetermined"] + st["n_nonfinite"] == n
+    rng = np.random.default_rng(9)
+    sel = np.unique(np.concatenate([rng.choice(n, 20000, replace=False), np.arange(n - 300, n)]))
+    sub_ids = torch.nonzero((f & 4) > 0).flatten()[:5000].cpu().numpy()
+    sel = np.unique(np.concatenate([sel, sub_ids]))
+    sel_t = torch.from_numpy(sel).cuda()
+    sample = coords.index_select(1, sel_t).cpu().numpy()
+    fs = f.index_select(0, sel_t).cpu().numpy()
+    del coords
+    torch.cuda.empty_cache()
+    ref = oracle.check_soa(sample)
+    assert_flags_match(fs, ref, allow_near=True)
+    assert ref["near"].sum() <= 2
