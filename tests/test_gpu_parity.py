@@ -651,3 +651,31 @@ def test_large_soa_input_sampled():
     ref = oracle.check_soa(sample)
     assert_flags_match(fs, ref, allow_near=True)
     assert ref["near"].sum() <= 2
+
+
+def test_large_indexed_input_sampled():
+    """n = 2^28 + 5 candidate hexes (8.6 GB of int32 connectivity): grid cells of a jittered
+    100^3 vertex grid chosen by a seeded device generator; sampled parity incl. the tail."""
+    n = (1 << 28) + 5
+    free, _ = torch.cuda.mem_get_info()
+    if free < 20e9:
+        pytest.skip("needs ~20 GB of free device memory")
+    verts = hexgen.grid_vertices(100, 0.2, 3)
+    g = torch.Generator(device="cuda").manual_seed(4321)
+    cells = torch.randint(0, 99 ** 3, (n,), generator=g, device="cuda", dtype=torch.int64)
+    ci, cj, ck = cells % 99, (cells // 99) % 99, cells // (99 * 99)
+    off = torch.from_numpy(pins.KAPPA.astype(np.int64)).cuda()
+    idx = ((ci[:, None] + off[None, :, 0]) + 100 * ((cj[:, None] + off[None, :, 1]) + 100 * (ck[:, None] + off[None, :, 2]))).to(torch.int32)
+    del cells, ci, cj, ck
+    v = torch.from_numpy(verts).cuda()
+    f, _ = hv.check_indexed(v, idx)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(10)
+    sel = np.unique(np.concatenate([rng.choice(n, 20000, replace=False), np.arange(n - 300, n)]))
+    sel_t = torch.from_numpy(sel).cuda()
+    idx_s = idx.index_select(0, sel_t).cpu().numpy()
+    fs = f.index_select(0, sel_t).cpu().numpy()
+    del idx
+    torch.cuda.empty_cache()
+    ref = oracle.check_indexed(verts, idx_s)
+    assert_flags_match(fs, ref)
