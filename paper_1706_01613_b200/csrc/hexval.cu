@@ -302,20 +302,19 @@ __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i
     return st;
 }
 
-template <class L, bool COEFFS, bool STATS>
-__global__ void __launch_bounds__(P1_THREADS, 2) pass1_kernel(L ld, int64_t n, uint8_t* __restrict__ flags,
-                                                           double* __restrict__ coeffs, Ctl* ctl,
-                                                           uint32_t* __restrict__ qsub,
-                                                           uint32_t* __restrict__ qexact,
-                                                           hexval_stats* stats) {
+// One hex per thread, plain loads: the fallback pass 1 (unaligned inputs,
+// HEXVAL_PASS1=ldg) and the NEXT-1 root phase.  Body: see Pass1Body.
+template <class L, class Body>
+__global__ void __launch_bounds__(P1_THREADS, 2) plain_kernel(L ld, int64_t n, Body body) {
     const int64_t i = (int64_t)blockIdx.x * P1_THREADS + threadIdx.x;
     int st = -1;
     if (i < n) {
         double X[24];
         ld.load_stream(i, X);
-        st = pass1_hex<COEFFS>(ld, X, i, n, flags, coeffs);
+        st = body.hex(ld, X, i);
     }
-    warp_epilogue<STATS>(st, i, ctl, qsub, qexact, stats);
+    body.epilogue(st, i);
+    body.finish();
 }
 
 // ---------------------------------------------------------------------------
@@ -466,17 +465,40 @@ __device__ __forceinline__ void cp_issue_hex(const double* __restrict__ coords, 
     cp_async_commit();                                        // (possibly empty) group per tile
 }
 
+// Per-hex bodies run by the pipelines below.  hex() runs on the lanes that
+// own a hex (X in registers) and returns a state; epilogue() is warp-collective
+// (every lane, st = -1 without a hex); finish() once per thread at the end.
 template <bool COEFFS, bool STATS>
+struct Pass1Body {                                           // K1/K2: S1-S8 + K3
+    int64_t n;
+    uint8_t* flags;
+    double* coeffs;
+    Ctl* ctl;
+    uint32_t* qsub;
+    uint32_t* qexact;
+    hexval_stats* stats;
+    P1Counts cnt;
+    template <class L>
+    __device__ __forceinline__ int hex(const L& ld, const double* X, int64_t i) {
+        return pass1_hex<COEFFS>(ld, X, i, n, flags, coeffs);
+    }
+    __device__ __forceinline__ void epilogue(int st, int64_t i) {
+        warp_epilogue<false>(st, i, ctl, qsub, qexact, stats);
+        if (STATS) cnt.add(st);
+    }
+    __device__ __forceinline__ void finish() {
+        if (STATS) cnt.flush(stats);
+    }
+};
+
+template <class Body>
 __global__ void __launch_bounds__(CP_THREADS, 2)
-    pass1_soa_cp_kernel(const double* __restrict__ coords, int64_t n, uint8_t* __restrict__ flags,
-                        double* __restrict__ coeffs, Ctl* ctl, uint32_t* __restrict__ qsub,
-                        uint32_t* __restrict__ qexact, hexval_stats* stats) {
+    soa_cp_kernel(const double* __restrict__ coords, int64_t n, Body body) {
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS]
     const int tid = threadIdx.x;
     const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
     const uint32_t s0 = smem_u32(cp_buf + tid);
     const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
-    P1Counts cnt;
     int64_t t = blockIdx.x;
     cp_issue_hex(coords, n, t * CP_THREADS + tid, s0);
     cp_issue_hex(coords, n, (t + gridDim.x) * CP_THREADS + tid, s1);
@@ -490,15 +512,14 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
             double X[24];
 #pragma unroll
             for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
-            st = pass1_hex<COEFFS>(SoaLoader{coords, n}, X, i, n, flags, coeffs);
+            st = body.hex(SoaLoader{coords, n}, X, i);
         }
         // refill this buffer with tile k+2 (X was consumed above: program order)
         cp_issue_hex(coords, n, (t + 2 * (int64_t)gridDim.x) * CP_THREADS + tid, b ? s1 : s0);
-        warp_epilogue<false>(st, i, ctl, qsub, qexact, stats);
-        if (STATS) cnt.add(st);
+        body.epilogue(st, i);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    if (STATS) cnt.flush(stats);
+    body.finish();
 }
 
 // K2 (cp.async variant): the same pipeline for int32 connectivity, three deep:
@@ -538,11 +559,9 @@ __device__ __forceinline__ void cp_gather_row(const double* __restrict__ verts, 
     }
 }
 
-template <bool COEFFS, bool STATS>
+template <class Body>
 __global__ void __launch_bounds__(CP_THREADS, 2)
-    pass1_idx_cp_kernel(const double* __restrict__ verts, const int32_t* __restrict__ idx, int64_t n,
-                        uint8_t* __restrict__ flags, double* __restrict__ coeffs, Ctl* ctl,
-                        uint32_t* __restrict__ qsub, uint32_t* __restrict__ qexact, hexval_stats* stats) {
+    idx_cp_kernel(const double* __restrict__ verts, const int32_t* __restrict__ idx, int64_t n, Body body) {
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS] coords, then [2][CP_THREADS][8] ids
     const int tid = threadIdx.x;
     const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
@@ -554,7 +573,6 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
     int32_t* const row1 = rows + 8 * (CP_THREADS + tid);      // ... odd k
     const uint32_t r0 = smem_u32(row0), r1 = smem_u32(row1);
     const IdxLoader ld{verts, idx};
-    P1Counts cnt;
     int64_t t = blockIdx.x;
     // prologue: rows of tiles 0 and 1 synchronously, then groups G0 = {gathers 0, row 2}, G1 = {gathers 1, row 3}
     cp_idx_row(idx, n, t * CP_THREADS + tid, r0);
@@ -576,17 +594,16 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
             double X[24];
 #pragma unroll
             for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
-            st = pass1_hex<COEFFS>(ld, X, i, n, flags, coeffs);
+            st = body.hex(ld, X, i);
         }
         // group k+2: gathers of tile k+2 (row read from shared memory), row of tile k+4
         cp_gather_row(verts, n, (t + 2 * G) * CP_THREADS + tid, bb ? row1 : row0, bb ? s1 : s0);
         cp_idx_row(idx, n, (t + 4 * G) * CP_THREADS + tid, bb ? r1 : r0);
         cp_async_commit();
-        warp_epilogue<false>(st, i, ctl, qsub, qexact, stats);
-        if (STATS) cnt.add(st);
+        body.epilogue(st, i);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    if (STATS) cnt.flush(stats);
+    body.finish();
 }
 
 // ---------------------------------------------------------------------------
@@ -705,6 +722,35 @@ __device__ __forceinline__ int stack_load(const double* sc, int slot, double* P)
     }
     return owner;
 }
+// Shared-memory mirror of a warp's most recent pushes (HEXVAL_K4_MIRROR): every
+// push also lands in entry slot mod 64; after a step that pushed, the next
+// step pops only this step's (<= 32) newest pushes, so it reads them here
+// instead of taking an L2 round trip.  Warp-uniform, no tags.
+constexpr int K4_MIR = 64;
+#ifdef HEXVAL_K4_MIRROR
+constexpr size_t K4_MIR_SMEM = (size_t)K4_WARPS * 14 * K4_MIR * sizeof(double2);
+#else
+constexpr size_t K4_MIR_SMEM = 0;
+#endif
+__device__ __forceinline__ int mirror_load(const double2* mir, int slot, double* P) {
+    const int e = slot & (K4_MIR - 1);
+    int owner = 0;
+#pragma unroll
+    for (int q = 0; q < 14; ++q) {
+        const double2 v = mir[q * K4_MIR + e];
+        P[2 * q] = v.x;
+        if (2 * q + 1 < 27) P[2 * q + 1] = v.y;
+        else owner = __double2loint(v.y);
+    }
+    return owner;
+}
+__device__ __forceinline__ void mirror_store(double2* mir, int slot, const double* C, int owner) {
+    const int e = slot & (K4_MIR - 1);
+#pragma unroll
+    for (int q = 0; q < 14; ++q)
+        mir[q * K4_MIR + e] = make_double2(C[2 * q], 2 * q + 1 < 27 ? C[2 * q + 1] : __hiloint2double(0, owner));
+}
+
 __device__ __forceinline__ void stack_store(double* sc, int slot, const double* C, int owner) {
     double2* s2 = reinterpret_cast<double2*>(sc);
 #pragma unroll
@@ -809,6 +855,11 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
                                                             const uint32_t* __restrict__ qexact, WarpStacks ws,
                                                             hexval_stats* stats) {
     __shared__ K4Warp wst[K4_WARPS];
+#ifdef HEXVAL_K4_MIRROR
+    extern __shared__ __align__(16) double2 k4_mir[];
+    double2* const mir = k4_mir + (size_t)(threadIdx.x >> 5) * 14 * K4_MIR;
+#endif
+    bool from_mirror = false;                          // warp-uniform: the previous step pushed
     const int lane = threadIdx.x & 31;
     K4Warp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
@@ -883,7 +934,11 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             d = D;
             if (act) {
                 const int slot = top - k + lane;
-                owner = stack_load(sc, slot, P);
+#ifdef HEXVAL_K4_MIRROR
+                if (from_mirror) owner = mirror_load(mir, slot, P);
+                else
+#endif
+                    owner = stack_load(sc, slot, P);
                 act = (W.status[owner] & 1u) == 0;       // hex already INVALID: drop the node
             }
             top -= k;
@@ -945,6 +1000,9 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
 #pragma unroll
                                     for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
                             stack_store(sc, slot, C, owner);
+#ifdef HEXVAL_K4_MIRROR
+                            mirror_store(mir, slot, C, owner);
+#endif
 
                         }
                     }
@@ -954,6 +1012,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
         if (inval) atomicOr(&W.status[owner], 1u);
         if (capped) atomicOr(&W.status[owner], 2u);
         top += pushed;
+        from_mirror = pushed > 0;
         __syncwarp();
         if (pushed) {
             if (lane == 0) W.cnt[d + 1] += pushed;
@@ -1033,17 +1092,18 @@ __device__ __forceinline__ double root_bounds(const double* P, double rel_tol, d
     return __dmul_rn(rel_tol, sc_);
 }
 
-template <class L>
-__global__ void __launch_bounds__(256) bounds_root_kernel(L ld, int64_t n, double rel_tol, double* __restrict__ lower_out,
-                                                           double* __restrict__ upper_out, uint8_t* __restrict__ status_out,
-                                                           unsigned* __restrict__ qcount, uint32_t* __restrict__ q) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool queue = false;
-    if (i < n) {
-        double X[24];
-        ld.load_stream(i, X);
+struct BoundsRootBody {
+    double rel_tol;
+    double* lower;
+    double* upper;
+    uint8_t* status;
+    unsigned* qcount;
+    uint32_t* q;
+    template <class L>
+    __device__ __forceinline__ int hex(const L&, const double* X, int64_t i) {
         double lo, up;
         uint8_t st = 0;
+        bool queue = false;
         if (out_of_range(X)) {
             lo = up = __longlong_as_double(0x7ff8000000000000ll);
             st = 2;                                          // NONFINITE
@@ -1060,13 +1120,15 @@ __global__ void __launch_bounds__(256) bounds_root_kernel(L ld, int64_t n, doubl
             queue = !(mn >= up - tol);
         }
         if (!queue) {
-            __stcs(lower_out + i, lo);
-            __stcs(upper_out + i, up);
-            if (status_out) __stcs(status_out + i, st);
+            __stcs(lower + i, lo);
+            __stcs(upper + i, up);
+            if (status) __stcs(status + i, st);
         }
+        return queue ? 1 : 0;
     }
-    warp_append(queue, (uint32_t)i, q, qcount);
-}
+    __device__ __forceinline__ void epilogue(int st, int64_t i) { warp_append(st == 1, (uint32_t)i, q, qcount); }
+    __device__ __forceinline__ void finish() {}
+};
 
 template <class L>
 __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restrict__ lower_out,
@@ -1074,6 +1136,11 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
                                                             unsigned* ctlq, const uint32_t* __restrict__ q, WarpStacks ws,
                                                             unsigned long long* nodes_out) {
     __shared__ BWarp wst[K4_WARPS];
+#ifdef HEXVAL_K4_MIRROR
+    extern __shared__ __align__(16) double2 k4_mir[];
+    double2* const mir = k4_mir + (size_t)(threadIdx.x >> 5) * 14 * K4_MIR;
+#endif
+    bool from_mirror = false;                          // warp-uniform: the previous step pushed
     const int lane = threadIdx.x & 31;
     BWarp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
@@ -1126,7 +1193,11 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
             d = D;
             if (lane < k) {
                 const int slot = top - k + lane;
-                owner = stack_load(sc, slot, P);
+#ifdef HEXVAL_K4_MIRROR
+                if (from_mirror) owner = mirror_load(mir, slot, P);
+                else
+#endif
+                    owner = stack_load(sc, slot, P);
                 // upper may have dropped since the push: the node may now be a leaf
                 double mn = P[0];
 #pragma unroll
@@ -1195,6 +1266,9 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
 #pragma unroll
                                     for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
                             stack_store(sc, slot, C, owner);
+#ifdef HEXVAL_K4_MIRROR
+                            mirror_store(mir, slot, C, owner);
+#endif
 
                         }
                     }
@@ -1202,6 +1276,7 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
                 }
             }
         top += pushed;
+        from_mirror = pushed > 0;
         __syncwarp();
         if (pushed) {
             if (lane == 0) W.cnt[d + 1] += pushed;
@@ -1444,20 +1519,24 @@ int wtma_setup() {
     return occ;
 }
 
+template <class Body>
+bool cp_attr(size_t smem_soa, size_t smem_idx) {
+    return cudaFuncSetAttribute((const void*)soa_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_soa) == cudaSuccess &&
+           cudaFuncSetAttribute((const void*)idx_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_idx) == cudaSuccess;
+}
+
 int cp_setup() {
-    const void* fns[8] = {(const void*)pass1_soa_cp_kernel<false, false>, (const void*)pass1_soa_cp_kernel<false, true>,
-                          (const void*)pass1_soa_cp_kernel<true, false>, (const void*)pass1_soa_cp_kernel<true, true>,
-                          (const void*)pass1_idx_cp_kernel<false, false>, (const void*)pass1_idx_cp_kernel<false, true>,
-                          (const void*)pass1_idx_cp_kernel<true, false>, (const void*)pass1_idx_cp_kernel<true, true>};
-    for (int f = 0; f < 8; ++f)
-        if (cudaFuncSetAttribute(fns[f], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(f < 4 ? CP_SMEM : CPI_SMEM)) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return 0;
-        }
+    const bool ok = cp_attr<Pass1Body<false, false>>(CP_SMEM, CPI_SMEM) && cp_attr<Pass1Body<false, true>>(CP_SMEM, CPI_SMEM) &&
+                    cp_attr<Pass1Body<true, false>>(CP_SMEM, CPI_SMEM) && cp_attr<Pass1Body<true, true>>(CP_SMEM, CPI_SMEM);
+    if (!ok) {
+        cudaGetLastError();
+        return 0;
+    }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass1_soa_cp_kernel<false, false>, CP_THREADS, CP_SMEM) !=
-        cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, soa_cp_kernel<Pass1Body<false, false>>, CP_THREADS,
+                                                      CP_SMEM) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -1482,7 +1561,18 @@ const DeviceInfo& device_info(int dev) {
     if (!d.ok) {
         cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false>, K4_THREADS, 0);
+        if (K4_MIR_SMEM) {
+            const void* k4fns[] = {(const void*)subdiv_kernel<CoordRoot<SoaLoader>, false>,
+                                   (const void*)subdiv_kernel<CoordRoot<SoaLoader>, true>,
+                                   (const void*)subdiv_kernel<CoordRoot<IdxLoader>, false>,
+                                   (const void*)subdiv_kernel<CoordRoot<IdxLoader>, true>,
+                                   (const void*)subdiv_kernel<CoeffRoot, false>, (const void*)subdiv_kernel<CoeffRoot, true>,
+                                   (const void*)bounds_kernel<SoaLoader>, (const void*)bounds_kernel<IdxLoader>};
+            for (const void* f : k4fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K4_MIR_SMEM);
+            cudaGetLastError();
+        }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false>, K4_THREADS,
+                                                      K4_MIR_SMEM);
         d.k4_blocks_per_sm = occ > 0 ? occ : 1;
         const int want = pass1_variant_from_env();
         const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup() : 0);
@@ -1516,11 +1606,11 @@ void launch_pass1_plain(const L& ld, int64_t n, uint8_t* flags, double* coeffs, 
                         uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
     const unsigned blocks = (unsigned)((n + P1_THREADS - 1) / P1_THREADS);
     if (coeffs) {
-        if (stats) pass1_kernel<L, true, true><<<blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_kernel<L, true, false><<<blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
+        if (stats) plain_kernel<<<blocks, P1_THREADS, 0, stream>>>(ld, n, Pass1Body<true, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else plain_kernel<<<blocks, P1_THREADS, 0, stream>>>(ld, n, Pass1Body<true, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
     } else {
-        if (stats) pass1_kernel<L, false, true><<<blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_kernel<L, false, false><<<blocks, P1_THREADS, 0, stream>>>(ld, n, flags, coeffs, ctl, qsub, qex, stats);
+        if (stats) plain_kernel<<<blocks, P1_THREADS, 0, stream>>>(ld, n, Pass1Body<false, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else plain_kernel<<<blocks, P1_THREADS, 0, stream>>>(ld, n, Pass1Body<false, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
     }
 }
 
@@ -1543,11 +1633,11 @@ void launch_pass1<IdxLoader>(const IdxLoader& ld, const DeviceInfo& info, int64_
     const double* v = ld.verts;
     const int32_t* x = ld.idx;
     if (coeffs) {
-        if (stats) pass1_idx_cp_kernel<true, true><<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_idx_cp_kernel<true, false><<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+        if (stats) idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, Pass1Body<true, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, Pass1Body<true, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
     } else {
-        if (stats) pass1_idx_cp_kernel<false, true><<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_idx_cp_kernel<false, false><<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, flags, coeffs, ctl, qsub, qex, stats);
+        if (stats) idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, Pass1Body<false, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, Pass1Body<false, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
     }
 }
 
@@ -1574,11 +1664,11 @@ void launch_cp(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* 
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
     const double* c = ld.coords;
     if (coeffs) {
-        if (stats) pass1_soa_cp_kernel<true, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_soa_cp_kernel<true, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+        if (stats) soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<true, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<true, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
     } else {
-        if (stats) pass1_soa_cp_kernel<false, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_soa_cp_kernel<false, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+        if (stats) soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<false, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<false, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
     }
 }
 
@@ -1597,8 +1687,17 @@ template <class R>
 void launch_subdiv(const R& root, const DeviceInfo& info, unsigned blocks, uint8_t* flags, Ctl* ctl,
                    const uint32_t* qsub, const uint32_t* qex, const WarpStacks& fr, hexval_stats* stats,
                    cudaStream_t stream) {
-    if (stats) subdiv_kernel<R, true><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
-    else subdiv_kernel<R, false><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
+    if (stats) subdiv_kernel<R, true><<<blocks, K4_THREADS, K4_MIR_SMEM, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
+    else subdiv_kernel<R, false><<<blocks, K4_THREADS, K4_MIR_SMEM, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
+}
+
+// Persistent K4 / bounds grid: one block per SM slot, but no more warps than
+// there can be batches of 32 queued hexes (the queue holds at most n), so a
+// small call does not reserve (or page in) stacks for idle warps.
+unsigned k4_grid(const DeviceInfo& info, int64_t n, int blocks_per_sm) {
+    const int64_t full = (int64_t)info.sms * blocks_per_sm;
+    const int64_t need = ((n + 31) / 32 + K4_WARPS - 1) / K4_WARPS;
+    return (unsigned)(need < full ? (need > 0 ? need : 1) : full);
 }
 
 int collect_profile(hexval_profile* p) {
@@ -1621,7 +1720,8 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return HEXVAL_ERR_CUDA;
     const DeviceInfo& info = device_info<L>(dev);
-    const size_t warps = (size_t)info.sms * info.k4_blocks_per_sm * K4_WARPS;
+    const unsigned k4_blocks = k4_grid(info, n, info.k4_blocks_per_sm);
+    const size_t warps = (size_t)k4_blocks * K4_WARPS;
 
     if (prof && prof->count >= hexval_profile::CAP) return HEXVAL_ERR_ARGUMENT;   // read it first
     const size_t ctl_bytes = 256;
@@ -1650,7 +1750,6 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     mark(HEXVAL_PHASE_PASS1, 1);
     // K5 (exact signs) is fused into K4's batch filling: no separate launch
     mark(HEXVAL_PHASE_SUBDIV, 0);
-    const unsigned k4_blocks = (unsigned)(info.sms * info.k4_blocks_per_sm);
     const CoordRoot<L> root{ld};
     launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, qex, fr, stats, stream);
     mark(HEXVAL_PHASE_SUBDIV, 1);
@@ -1696,7 +1795,8 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return HEXVAL_ERR_CUDA;
     const DeviceInfo& info = device_info<SoaLoader>(dev);
-    const size_t warps = (size_t)info.sms * info.k4_blocks_per_sm * K4_WARPS;
+    const unsigned k4_blocks = k4_grid(info, n, info.k4_blocks_per_sm);
+    const size_t warps = (size_t)k4_blocks * K4_WARPS;
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
@@ -1714,11 +1814,17 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     if (stats) bezier_pass_kernel<true><<<p1_blocks, P1_THREADS, 0, stream>>>(b, n, flags, ctl, qsub, stats);
     else bezier_pass_kernel<false><<<p1_blocks, P1_THREADS, 0, stream>>>(b, n, flags, ctl, qsub, stats);
     const CoeffRoot root{b, n};
-    const unsigned k4_blocks = (unsigned)(info.sms * info.k4_blocks_per_sm);
     launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, qsub, fr, stats, stream);
     cudaFreeAsync(base, stream);
     if (cudaGetLastError() != cudaSuccess) return HEXVAL_ERR_CUDA;
     return HEXVAL_OK;
+}
+
+// NEXT-1 root phase: the plain one-hex-per-thread kernel (measured: 0.853 vs
+// 0.867 ms on config 1, 4.01 vs 4.14 ms on config 3 for the cp.async pipeline)
+template <class L>
+void launch_bounds_root(const L& ld, int64_t n, const BoundsRootBody& body, cudaStream_t stream) {
+    plain_kernel<<<(unsigned)((n + P1_THREADS - 1) / P1_THREADS), P1_THREADS, 0, stream>>>(ld, n, body);
 }
 
 template <class L>
@@ -1729,9 +1835,9 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     if (cudaGetDevice(&dev) != cudaSuccess) return HEXVAL_ERR_CUDA;
     const DeviceInfo& info = device_info<SoaLoader>(dev);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bounds_kernel<L>, K4_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bounds_kernel<L>, K4_THREADS, K4_MIR_SMEM);
     if (occ < 1) occ = 1;
-    const int64_t blocks = (int64_t)info.sms * occ;
+    const int64_t blocks = k4_grid(info, n, occ);
     const size_t warps = (size_t)blocks * K4_WARPS;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
@@ -1745,8 +1851,8 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     WarpStacks ws;
     ws.coef = reinterpret_cast<double*>(base + 256 + q_bytes);
     cudaMemsetAsync(ctlq, 0, 256, stream);
-    bounds_root_kernel<L><<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(ld, n, rel_tol, lower, upper, status, ctlq, q);
-    bounds_kernel<L><<<(unsigned)blocks, K4_THREADS, 0, stream>>>(ld, rel_tol, lower, upper, status, ctlq, q, ws,
+    launch_bounds_root(ld, n, BoundsRootBody{rel_tol, lower, upper, status, ctlq, q}, stream);
+    bounds_kernel<L><<<(unsigned)blocks, K4_THREADS, K4_MIR_SMEM, stream>>>(ld, rel_tol, lower, upper, status, ctlq, q, ws,
                                                                     nodes_dev_opt);
     cudaFreeAsync(base, stream);
     return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
@@ -2049,7 +2155,7 @@ const char* hexval_status_string(int status) {
     }
 }
 
-int hexval_version(void) { return 100; }
+int hexval_version(void) { return 110; }
 
 int hexval_kernel_launches_per_call(void) { return 2; }
 
