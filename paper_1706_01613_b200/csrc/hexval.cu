@@ -123,13 +123,12 @@ struct IdxLoader {
 
 // NONFINITE (reading G13): a coordinate is NaN/Inf or |x| > 2^300
 __device__ __forceinline__ bool out_of_range(const double* X) {
-#ifdef HEXVAL_KEYS_V2
-    // max |hi word| without masking: signed max covers x >= 0, unsigned max x < 0
-    int sm = 0x80000000;
-    unsigned um = 0;
+#ifdef HEXVAL_KEY_TREE
+    int m[8];
 #pragma unroll
-    for (int p = 0; p < 24; ++p) { sm = max(sm, key(X[p])); um = max(um, (unsigned)key(X[p])); }
-    if (sm < 0x52B00000 && um < 0xD2B00000u) return false;   // every |x| < 2^300
+    for (int k = 0; k < 8; ++k) m[k] = max(abskey(X[3 * k]), max(abskey(X[3 * k + 1]), abskey(X[3 * k + 2])));
+    const int mk = max(max(max(m[0], m[1]), max(m[2], m[3])), max(max(m[4], m[5]), max(m[6], m[7])));
+    if (mk < 0x52B00000) return false;                 // every |x| < 2^300
 #else
     int mk = 0;
 #pragma unroll
@@ -465,6 +464,27 @@ __device__ __forceinline__ void cp_issue_hex(const double* __restrict__ coords, 
     cp_async_commit();                                        // (possibly empty) group per tile
 }
 
+// Lane pairs (2j, 2j+1) share the copies of their two hexes: each lane issues
+// 12 16-byte copies (planes 12h .. 12h+11 for both hexes, h = lane & 1) instead
+// of 24 8-byte ones.  Needs n even (then plane p of hex pair 2j starts 16-B
+// aligned); the pair's tail (2j+1 >= n) falls back to one 8-byte copy.
+__device__ __forceinline__ void cp_issue_pair(const double* __restrict__ coords, int64_t n, int64_t i0, int half,
+                                              uint32_t dst_pair) {
+    if (i0 < n) {
+        const uint64_t policy = policy_evict_first();
+        const bool both = i0 + 1 < n;
+#pragma unroll
+        for (int q = 0; q < 12; ++q) {
+            const int p = 12 * half + q;
+            const double* src = coords + (int64_t)p * n + i0;
+            const uint32_t dst = dst_pair + p * CP_THREADS * 8;
+            if (both) asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(policy) : "memory");
+            else cp_async8(dst, src, policy);
+        }
+    }
+    cp_async_commit();
+}
+
 // Per-hex bodies run by the pipelines below.  hex() runs on the lanes that
 // own a hex (X in registers) and returns a state; epilogue() is warp-collective
 // (every lane, st = -1 without a hex); finish() once per thread at the end.
@@ -491,7 +511,7 @@ struct Pass1Body {                                           // K1/K2: S1-S8 + K
     }
 };
 
-template <class Body>
+template <class Body, bool PAIR>
 __global__ void __launch_bounds__(CP_THREADS, 2)
     soa_cp_kernel(const double* __restrict__ coords, int64_t n, Body body) {
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS]
@@ -499,23 +519,34 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
     const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
     const uint32_t s0 = smem_u32(cp_buf + tid);
     const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
+    const uint32_t p0 = smem_u32(cp_buf + (tid & ~1)), p1 = p0 + 24 * CP_THREADS * 8;   // PAIR: the pair's base
+    const int half = tid & 1;
+    auto issue = [&](int64_t tile, int b) {
+        if (PAIR) cp_issue_pair(coords, n, tile * CP_THREADS + (tid & ~1), half, b ? p1 : p0);
+        else cp_issue_hex(coords, n, tile * CP_THREADS + tid, b ? s1 : s0);
+    };
     int64_t t = blockIdx.x;
-    cp_issue_hex(coords, n, t * CP_THREADS + tid, s0);
-    cp_issue_hex(coords, n, (t + gridDim.x) * CP_THREADS + tid, s1);
+    issue(t, 0);
+    issue(t + gridDim.x, 1);
     for (int k = 0; t < tiles; t += gridDim.x, ++k) {
         const int b = k & 1;
         cp_async_wait1();                                    // tile k has landed (tile k+1 may be in flight)
+        if (PAIR) __syncwarp();                              // ... including the partner lane's copies
         const int64_t i = t * CP_THREADS + tid;
         int st = -1;
+        double X[24];
         if (i < n) {
             const double* src = cp_buf + b * 24 * CP_THREADS + tid;
-            double X[24];
 #pragma unroll
             for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
-            st = body.hex(SoaLoader{coords, n}, X, i);
         }
+        if (PAIR) {
+            __syncwarp();                                    // both lanes of the pair have read buffer b
+            issue(t + 2 * (int64_t)gridDim.x, b);
+        }
+        if (i < n) st = body.hex(SoaLoader{coords, n}, X, i);
         // refill this buffer with tile k+2 (X was consumed above: program order)
-        cp_issue_hex(coords, n, (t + 2 * (int64_t)gridDim.x) * CP_THREADS + tid, b ? s1 : s0);
+        if (!PAIR) issue(t + 2 * (int64_t)gridDim.x, b);
         body.epilogue(st, i);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -722,35 +753,6 @@ __device__ __forceinline__ int stack_load(const double* sc, int slot, double* P)
     }
     return owner;
 }
-// Shared-memory mirror of a warp's most recent pushes (HEXVAL_K4_MIRROR): every
-// push also lands in entry slot mod 64; after a step that pushed, the next
-// step pops only this step's (<= 32) newest pushes, so it reads them here
-// instead of taking an L2 round trip.  Warp-uniform, no tags.
-constexpr int K4_MIR = 64;
-#ifdef HEXVAL_K4_MIRROR
-constexpr size_t K4_MIR_SMEM = (size_t)K4_WARPS * 14 * K4_MIR * sizeof(double2);
-#else
-constexpr size_t K4_MIR_SMEM = 0;
-#endif
-__device__ __forceinline__ int mirror_load(const double2* mir, int slot, double* P) {
-    const int e = slot & (K4_MIR - 1);
-    int owner = 0;
-#pragma unroll
-    for (int q = 0; q < 14; ++q) {
-        const double2 v = mir[q * K4_MIR + e];
-        P[2 * q] = v.x;
-        if (2 * q + 1 < 27) P[2 * q + 1] = v.y;
-        else owner = __double2loint(v.y);
-    }
-    return owner;
-}
-__device__ __forceinline__ void mirror_store(double2* mir, int slot, const double* C, int owner) {
-    const int e = slot & (K4_MIR - 1);
-#pragma unroll
-    for (int q = 0; q < 14; ++q)
-        mir[q * K4_MIR + e] = make_double2(C[2 * q], 2 * q + 1 < 27 ? C[2 * q + 1] : __hiloint2double(0, owner));
-}
-
 __device__ __forceinline__ void stack_store(double* sc, int slot, const double* C, int owner) {
     double2* s2 = reinterpret_cast<double2*>(sc);
 #pragma unroll
@@ -855,11 +857,6 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
                                                             const uint32_t* __restrict__ qexact, WarpStacks ws,
                                                             hexval_stats* stats) {
     __shared__ K4Warp wst[K4_WARPS];
-#ifdef HEXVAL_K4_MIRROR
-    extern __shared__ __align__(16) double2 k4_mir[];
-    double2* const mir = k4_mir + (size_t)(threadIdx.x >> 5) * 14 * K4_MIR;
-#endif
-    bool from_mirror = false;                          // warp-uniform: the previous step pushed
     const int lane = threadIdx.x & 31;
     K4Warp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
@@ -934,11 +931,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             d = D;
             if (act) {
                 const int slot = top - k + lane;
-#ifdef HEXVAL_K4_MIRROR
-                if (from_mirror) owner = mirror_load(mir, slot, P);
-                else
-#endif
-                    owner = stack_load(sc, slot, P);
+                owner = stack_load(sc, slot, P);
                 act = (W.status[owner] & 1u) == 0;       // hex already INVALID: drop the node
             }
             top -= k;
@@ -1000,9 +993,6 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
 #pragma unroll
                                     for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
                             stack_store(sc, slot, C, owner);
-#ifdef HEXVAL_K4_MIRROR
-                            mirror_store(mir, slot, C, owner);
-#endif
 
                         }
                     }
@@ -1012,7 +1002,6 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
         if (inval) atomicOr(&W.status[owner], 1u);
         if (capped) atomicOr(&W.status[owner], 2u);
         top += pushed;
-        from_mirror = pushed > 0;
         __syncwarp();
         if (pushed) {
             if (lane == 0) W.cnt[d + 1] += pushed;
@@ -1136,11 +1125,6 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
                                                             unsigned* ctlq, const uint32_t* __restrict__ q, WarpStacks ws,
                                                             unsigned long long* nodes_out) {
     __shared__ BWarp wst[K4_WARPS];
-#ifdef HEXVAL_K4_MIRROR
-    extern __shared__ __align__(16) double2 k4_mir[];
-    double2* const mir = k4_mir + (size_t)(threadIdx.x >> 5) * 14 * K4_MIR;
-#endif
-    bool from_mirror = false;                          // warp-uniform: the previous step pushed
     const int lane = threadIdx.x & 31;
     BWarp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
@@ -1193,11 +1177,7 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
             d = D;
             if (lane < k) {
                 const int slot = top - k + lane;
-#ifdef HEXVAL_K4_MIRROR
-                if (from_mirror) owner = mirror_load(mir, slot, P);
-                else
-#endif
-                    owner = stack_load(sc, slot, P);
+                owner = stack_load(sc, slot, P);
                 // upper may have dropped since the push: the node may now be a leaf
                 double mn = P[0];
 #pragma unroll
@@ -1266,9 +1246,6 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
 #pragma unroll
                                     for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
                             stack_store(sc, slot, C, owner);
-#ifdef HEXVAL_K4_MIRROR
-                            mirror_store(mir, slot, C, owner);
-#endif
 
                         }
                     }
@@ -1276,7 +1253,6 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
                 }
             }
         top += pushed;
-        from_mirror = pushed > 0;
         __syncwarp();
         if (pushed) {
             if (lane == 0) W.cnt[d + 1] += pushed;
@@ -1493,6 +1469,7 @@ struct DeviceInfo {
     int sms = 0;
     int k4_blocks_per_sm = 0;
     int p1_variant = 0;           // SoA pass 1: P1_LDG (plain), P1_WTMA or P1_CP
+    bool p1_pair = false;         // P1_CP with lane-pair 16-byte copies when n is even (HEXVAL_PASS1=cp2)
     int p1_ctas_per_sm = 1;
     bool ok = false;
 };
@@ -1521,7 +1498,9 @@ int wtma_setup() {
 
 template <class Body>
 bool cp_attr(size_t smem_soa, size_t smem_idx) {
-    return cudaFuncSetAttribute((const void*)soa_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute((const void*)soa_cp_kernel<Body, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_soa) == cudaSuccess &&
+           cudaFuncSetAttribute((const void*)soa_cp_kernel<Body, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem_soa) == cudaSuccess &&
            cudaFuncSetAttribute((const void*)idx_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem_idx) == cudaSuccess;
@@ -1535,7 +1514,7 @@ int cp_setup() {
         return 0;
     }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, soa_cp_kernel<Pass1Body<false, false>>, CP_THREADS,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, soa_cp_kernel<Pass1Body<false, false>, false>, CP_THREADS,
                                                       CP_SMEM) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -1550,6 +1529,7 @@ int pass1_variant_from_env() {
     const char* v = getenv("HEXVAL_PASS1");
     if (v && !strcmp(v, "wtma")) return P1_WTMA;
     if (v && !strcmp(v, "cp")) return P1_CP;
+    if (v && !strcmp(v, "cp2")) return P1_CP;
     if (v && !strcmp(v, "ldg")) return P1_LDG;
     return P1_CP;                 // measured best on B200 (profiles/r01)
 }
@@ -1561,22 +1541,16 @@ const DeviceInfo& device_info(int dev) {
     if (!d.ok) {
         cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
         int occ = 0;
-        if (K4_MIR_SMEM) {
-            const void* k4fns[] = {(const void*)subdiv_kernel<CoordRoot<SoaLoader>, false>,
-                                   (const void*)subdiv_kernel<CoordRoot<SoaLoader>, true>,
-                                   (const void*)subdiv_kernel<CoordRoot<IdxLoader>, false>,
-                                   (const void*)subdiv_kernel<CoordRoot<IdxLoader>, true>,
-                                   (const void*)subdiv_kernel<CoeffRoot, false>, (const void*)subdiv_kernel<CoeffRoot, true>,
-                                   (const void*)bounds_kernel<SoaLoader>, (const void*)bounds_kernel<IdxLoader>};
-            for (const void* f : k4fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K4_MIR_SMEM);
-            cudaGetLastError();
-        }
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false>, K4_THREADS,
-                                                      K4_MIR_SMEM);
+                                                      0);
         d.k4_blocks_per_sm = occ > 0 ? occ : 1;
         const int want = pass1_variant_from_env();
         const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup() : 0);
         d.p1_variant = ctas > 0 ? want : P1_LDG;
+        {
+            const char* v = getenv("HEXVAL_PASS1");
+            d.p1_pair = v && !strcmp(v, "cp2");
+        }
         d.p1_ctas_per_sm = ctas > 0 ? ctas : 1;
         // keep freed stream-ordered scratch in the pool between calls
         cudaMemPool_t pool;
@@ -1663,12 +1637,22 @@ void launch_cp(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* 
     const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
     const double* c = ld.coords;
+    if (info.p1_pair && (n & 1) == 0 && (((uintptr_t)c) & 15) == 0) {
+        if (coeffs) {
+            if (stats) soa_cp_kernel<Pass1Body<true, true>, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
+            else soa_cp_kernel<Pass1Body<true, false>, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        } else {
+            if (stats) soa_cp_kernel<Pass1Body<false, true>, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
+            else soa_cp_kernel<Pass1Body<false, false>, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        }
+        return;
+    }
     if (coeffs) {
-        if (stats) soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<true, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<true, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        if (stats) soa_cp_kernel<Pass1Body<true, true>, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else soa_cp_kernel<Pass1Body<true, false>, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
     } else {
-        if (stats) soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<false, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<false, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        if (stats) soa_cp_kernel<Pass1Body<false, true>, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else soa_cp_kernel<Pass1Body<false, false>, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
     }
 }
 
@@ -1687,8 +1671,8 @@ template <class R>
 void launch_subdiv(const R& root, const DeviceInfo& info, unsigned blocks, uint8_t* flags, Ctl* ctl,
                    const uint32_t* qsub, const uint32_t* qex, const WarpStacks& fr, hexval_stats* stats,
                    cudaStream_t stream) {
-    if (stats) subdiv_kernel<R, true><<<blocks, K4_THREADS, K4_MIR_SMEM, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
-    else subdiv_kernel<R, false><<<blocks, K4_THREADS, K4_MIR_SMEM, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
+    if (stats) subdiv_kernel<R, true><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
+    else subdiv_kernel<R, false><<<blocks, K4_THREADS, 0, stream>>>(root, flags, ctl, qsub, qex, fr, stats);
 }
 
 // Persistent K4 / bounds grid: one block per SM slot, but no more warps than
@@ -1835,7 +1819,7 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     if (cudaGetDevice(&dev) != cudaSuccess) return HEXVAL_ERR_CUDA;
     const DeviceInfo& info = device_info<SoaLoader>(dev);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bounds_kernel<L>, K4_THREADS, K4_MIR_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bounds_kernel<L>, K4_THREADS, 0);
     if (occ < 1) occ = 1;
     const int64_t blocks = k4_grid(info, n, occ);
     const size_t warps = (size_t)blocks * K4_WARPS;
@@ -1852,7 +1836,7 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     ws.coef = reinterpret_cast<double*>(base + 256 + q_bytes);
     cudaMemsetAsync(ctlq, 0, 256, stream);
     launch_bounds_root(ld, n, BoundsRootBody{rel_tol, lower, upper, status, ctlq, q}, stream);
-    bounds_kernel<L><<<(unsigned)blocks, K4_THREADS, K4_MIR_SMEM, stream>>>(ld, rel_tol, lower, upper, status, ctlq, q, ws,
+    bounds_kernel<L><<<(unsigned)blocks, K4_THREADS, 0, stream>>>(ld, rel_tol, lower, upper, status, ctlq, q, ws,
                                                                     nodes_dev_opt);
     cudaFreeAsync(base, stream);
     return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;

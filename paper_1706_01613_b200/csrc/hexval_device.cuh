@@ -66,18 +66,15 @@ __device__ __forceinline__ void samples20(const double* X, Samples& s) {
     const V3 v12 = vsub(n2, n1), v43 = vsub(n3, n4), v56 = vsub(n6, n5), v87 = vsub(n7, n8);
     const V3 v14 = vsub(n4, n1), v23 = vsub(n3, n2), v58 = vsub(n8, n5), v67 = vsub(n7, n6);
     const V3 v15 = vsub(n5, n1), v26 = vsub(n6, n2), v48 = vsub(n8, n4), v37 = vsub(n7, n3);
-#ifdef HEXVAL_KEYS_V2
-    // max |hi word| of the 36 components: signed max covers components >= 0,
-    // unsigned max (sign bit set = largest) covers negative ones
-    int sm = 0x80000000;
-    unsigned um = 0;
-#define HV_EK(v) sm = max(sm, max(key(v.x), max(key(v.y), key(v.z)))); \
-                 um = max(um, max((unsigned)key(v.x), max((unsigned)key(v.y), (unsigned)key(v.z))))
-    HV_EK(v12); HV_EK(v43); HV_EK(v56); HV_EK(v87);
-    HV_EK(v14); HV_EK(v23); HV_EK(v58); HV_EK(v67);
-    HV_EK(v15); HV_EK(v26); HV_EK(v48); HV_EK(v37);
-#undef HV_EK
-    s.ekey = max(sm, (int)(um & 0x7fffffffu));
+#ifdef HEXVAL_KEY_TREE
+    // balanced: per-vector max of 3, then a 3-ary tree over the 12 vectors
+    int m[12];
+    const V3* vs[12] = {&v12, &v43, &v56, &v87, &v14, &v23, &v58, &v67, &v15, &v26, &v48, &v37};
+#pragma unroll
+    for (int q = 0; q < 12; ++q) m[q] = max(abskey(vs[q]->x), max(abskey(vs[q]->y), abskey(vs[q]->z)));
+    const int m0 = max(m[0], max(m[1], m[2])), m1 = max(m[3], max(m[4], m[5]));
+    const int m2 = max(m[6], max(m[7], m[8])), m3 = max(m[9], max(m[10], m[11]));
+    s.ekey = max(max(m0, m1), max(m2, m3));
 #else
     int e = 0;
 #define HV_EK(v) e = max(e, max(abskey(v.x), max(abskey(v.y), abskey(v.z))))
