@@ -123,10 +123,18 @@ struct IdxLoader {
 
 // NONFINITE (reading G13): a coordinate is NaN/Inf or |x| > 2^300
 __device__ __forceinline__ bool out_of_range(const double* X) {
+#ifdef HEXVAL_KEY_TREE
+    int m[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = max(abskey(X[3 * k]), max(abskey(X[3 * k + 1]), abskey(X[3 * k + 2])));
+    const int mk = max(max(max(m[0], m[1]), max(m[2], m[3])), max(max(m[4], m[5]), max(m[6], m[7])));
+    if (mk < 0x52B00000) return false;                 // every |x| < 2^300
+#else
     int mk = 0;
 #pragma unroll
     for (int p = 0; p < 24; ++p) mk = max(mk, abskey(X[p]));
     if (mk < 0x52B00000) return false;                 // every |x| < 2^300
+#endif
     bool bad = false;
 #pragma unroll
     for (int p = 0; p < 24; ++p) bad |= !(fabs(X[p]) <= 0x1p300);
@@ -526,16 +534,19 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
         if (PAIR) __syncwarp();                              // ... including the partner lane's copies
         const int64_t i = t * CP_THREADS + tid;
         int st = -1;
+        double X[24];
         if (i < n) {
             const double* src = cp_buf + b * 24 * CP_THREADS + tid;
-            double X[24];
 #pragma unroll
             for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
-            st = body.hex(SoaLoader{coords, n}, X, i);
         }
-        if (PAIR) __syncwarp();                              // both lanes of each pair have consumed buffer b
+        if (PAIR) {
+            __syncwarp();                                    // both lanes of the pair have read buffer b
+            issue(t + 2 * (int64_t)gridDim.x, b);
+        }
+        if (i < n) st = body.hex(SoaLoader{coords, n}, X, i);
         // refill this buffer with tile k+2 (X was consumed above: program order)
-        issue(t + 2 * (int64_t)gridDim.x, b);
+        if (!PAIR) issue(t + 2 * (int64_t)gridDim.x, b);
         body.epilogue(st, i);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");

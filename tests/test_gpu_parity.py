@@ -161,11 +161,10 @@ def test_misaligned_base_uses_plain_path_with_same_results():
 
 
 def test_pass1_variants_bit_identical(tmp_path):
-    """HEXVAL_PASS1=ldg|wtma|cp|cp2 (tuning knob) give identical flags and coefficients (n even, so
-    cp2's lane-pair 16-byte copies are used)."""
+    """HEXVAL_PASS1=ldg|wtma|cp (tuning knob) give identical flags and coefficients."""
     import subprocess
     import sys
-    n = 256 * 148 * 2 + 78
+    n = 256 * 148 * 2 + 77
     coords = hexgen.ragged_soa(n, seed=5, amp=0.5)
     np.save(tmp_path / "c.npy", coords)
     script = (
@@ -176,11 +175,11 @@ def test_pass1_variants_bit_identical(tmp_path):
         "f, k = hv.check_soa(c, coeffs=True); torch.cuda.synchronize()\n"
         f"np.save({str(tmp_path)!r} + '/f_' + sys.argv[1] + '.npy', f.cpu().numpy())\n"
         f"np.save({str(tmp_path)!r} + '/k_' + sys.argv[1] + '.npy', k.cpu().numpy())\n")
-    for v in ("ldg", "wtma", "cp", "cp2"):
+    for v in ("ldg", "wtma", "cp"):
         env = dict(os.environ, HEXVAL_PASS1=v)
         subprocess.run([sys.executable, "-c", script, v], env=env, check=True, timeout=300)
     f0, k0 = np.load(tmp_path / "f_ldg.npy"), np.load(tmp_path / "k_ldg.npy")
-    for v in ("wtma", "cp", "cp2"):
+    for v in ("wtma", "cp"):
         assert np.array_equal(np.load(tmp_path / f"f_{v}.npy"), f0), v
         assert np.array_equal(np.load(tmp_path / f"k_{v}.npy"), k0), v
 
