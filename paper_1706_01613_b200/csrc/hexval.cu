@@ -123,18 +123,10 @@ struct IdxLoader {
 
 // NONFINITE (reading G13): a coordinate is NaN/Inf or |x| > 2^300
 __device__ __forceinline__ bool out_of_range(const double* X) {
-#ifdef HEXVAL_KEY_TREE
-    int m[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) m[k] = max(abskey(X[3 * k]), max(abskey(X[3 * k + 1]), abskey(X[3 * k + 2])));
-    const int mk = max(max(max(m[0], m[1]), max(m[2], m[3])), max(max(m[4], m[5]), max(m[6], m[7])));
-    if (mk < 0x52B00000) return false;                 // every |x| < 2^300
-#else
     int mk = 0;
 #pragma unroll
     for (int p = 0; p < 24; ++p) mk = max(mk, abskey(X[p]));
     if (mk < 0x52B00000) return false;                 // every |x| < 2^300
-#endif
     bool bad = false;
 #pragma unroll
     for (int p = 0; p < 24; ++p) bad |= !(fabs(X[p]) <= 0x1p300);
@@ -464,27 +456,6 @@ __device__ __forceinline__ void cp_issue_hex(const double* __restrict__ coords, 
     cp_async_commit();                                        // (possibly empty) group per tile
 }
 
-// Lane pairs (2j, 2j+1) share the copies of their two hexes: each lane issues
-// 12 16-byte copies (planes 12h .. 12h+11 for both hexes, h = lane & 1) instead
-// of 24 8-byte ones.  Needs n even (then plane p of hex pair 2j starts 16-B
-// aligned); the pair's tail (2j+1 >= n) falls back to one 8-byte copy.
-__device__ __forceinline__ void cp_issue_pair(const double* __restrict__ coords, int64_t n, int64_t i0, int half,
-                                              uint32_t dst_pair) {
-    if (i0 < n) {
-        const uint64_t policy = policy_evict_first();
-        const bool both = i0 + 1 < n;
-#pragma unroll
-        for (int q = 0; q < 12; ++q) {
-            const int p = 12 * half + q;
-            const double* src = coords + (int64_t)p * n + i0;
-            const uint32_t dst = dst_pair + p * CP_THREADS * 8;
-            if (both) asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(policy) : "memory");
-            else cp_async8(dst, src, policy);
-        }
-    }
-    cp_async_commit();
-}
-
 // Per-hex bodies run by the pipelines below.  hex() runs on the lanes that
 // own a hex (X in registers) and returns a state; epilogue() is warp-collective
 // (every lane, st = -1 without a hex); finish() once per thread at the end.
@@ -511,7 +482,7 @@ struct Pass1Body {                                           // K1/K2: S1-S8 + K
     }
 };
 
-template <class Body, bool PAIR>
+template <class Body>
 __global__ void __launch_bounds__(CP_THREADS, 2)
     soa_cp_kernel(const double* __restrict__ coords, int64_t n, Body body) {
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS]
@@ -519,34 +490,23 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
     const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
     const uint32_t s0 = smem_u32(cp_buf + tid);
     const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
-    const uint32_t p0 = smem_u32(cp_buf + (tid & ~1)), p1 = p0 + 24 * CP_THREADS * 8;   // PAIR: the pair's base
-    const int half = tid & 1;
-    auto issue = [&](int64_t tile, int b) {
-        if (PAIR) cp_issue_pair(coords, n, tile * CP_THREADS + (tid & ~1), half, b ? p1 : p0);
-        else cp_issue_hex(coords, n, tile * CP_THREADS + tid, b ? s1 : s0);
-    };
     int64_t t = blockIdx.x;
-    issue(t, 0);
-    issue(t + gridDim.x, 1);
+    cp_issue_hex(coords, n, t * CP_THREADS + tid, s0);
+    cp_issue_hex(coords, n, (t + gridDim.x) * CP_THREADS + tid, s1);
     for (int k = 0; t < tiles; t += gridDim.x, ++k) {
         const int b = k & 1;
         cp_async_wait1();                                    // tile k has landed (tile k+1 may be in flight)
-        if (PAIR) __syncwarp();                              // ... including the partner lane's copies
         const int64_t i = t * CP_THREADS + tid;
         int st = -1;
-        double X[24];
         if (i < n) {
             const double* src = cp_buf + b * 24 * CP_THREADS + tid;
+            double X[24];
 #pragma unroll
             for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
+            st = body.hex(SoaLoader{coords, n}, X, i);
         }
-        if (PAIR) {
-            __syncwarp();                                    // both lanes of the pair have read buffer b
-            issue(t + 2 * (int64_t)gridDim.x, b);
-        }
-        if (i < n) st = body.hex(SoaLoader{coords, n}, X, i);
         // refill this buffer with tile k+2 (X was consumed above: program order)
-        if (!PAIR) issue(t + 2 * (int64_t)gridDim.x, b);
+        cp_issue_hex(coords, n, (t + 2 * (int64_t)gridDim.x) * CP_THREADS + tid, b ? s1 : s0);
         body.epilogue(st, i);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -1469,7 +1429,6 @@ struct DeviceInfo {
     int sms = 0;
     int k4_blocks_per_sm = 0;
     int p1_variant = 0;           // SoA pass 1: P1_LDG (plain), P1_WTMA or P1_CP
-    bool p1_pair = false;         // P1_CP with lane-pair 16-byte copies when n is even (HEXVAL_PASS1=cp2)
     int p1_ctas_per_sm = 1;
     bool ok = false;
 };
@@ -1498,9 +1457,7 @@ int wtma_setup() {
 
 template <class Body>
 bool cp_attr(size_t smem_soa, size_t smem_idx) {
-    return cudaFuncSetAttribute((const void*)soa_cp_kernel<Body, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_soa) == cudaSuccess &&
-           cudaFuncSetAttribute((const void*)soa_cp_kernel<Body, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute((const void*)soa_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem_soa) == cudaSuccess &&
            cudaFuncSetAttribute((const void*)idx_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem_idx) == cudaSuccess;
@@ -1514,7 +1471,7 @@ int cp_setup() {
         return 0;
     }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, soa_cp_kernel<Pass1Body<false, false>, false>, CP_THREADS,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, soa_cp_kernel<Pass1Body<false, false>>, CP_THREADS,
                                                       CP_SMEM) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -1529,7 +1486,6 @@ int pass1_variant_from_env() {
     const char* v = getenv("HEXVAL_PASS1");
     if (v && !strcmp(v, "wtma")) return P1_WTMA;
     if (v && !strcmp(v, "cp")) return P1_CP;
-    if (v && !strcmp(v, "cp2")) return P1_CP;
     if (v && !strcmp(v, "ldg")) return P1_LDG;
     return P1_CP;                 // measured best on B200 (profiles/r01)
 }
@@ -1547,10 +1503,6 @@ const DeviceInfo& device_info(int dev) {
         const int want = pass1_variant_from_env();
         const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup() : 0);
         d.p1_variant = ctas > 0 ? want : P1_LDG;
-        {
-            const char* v = getenv("HEXVAL_PASS1");
-            d.p1_pair = v && !strcmp(v, "cp2");
-        }
         d.p1_ctas_per_sm = ctas > 0 ? ctas : 1;
         // keep freed stream-ordered scratch in the pool between calls
         cudaMemPool_t pool;
@@ -1637,22 +1589,12 @@ void launch_cp(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* 
     const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
     const double* c = ld.coords;
-    if (info.p1_pair && (n & 1) == 0 && (((uintptr_t)c) & 15) == 0) {
-        if (coeffs) {
-            if (stats) soa_cp_kernel<Pass1Body<true, true>, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
-            else soa_cp_kernel<Pass1Body<true, false>, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        } else {
-            if (stats) soa_cp_kernel<Pass1Body<false, true>, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
-            else soa_cp_kernel<Pass1Body<false, false>, true><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        }
-        return;
-    }
     if (coeffs) {
-        if (stats) soa_cp_kernel<Pass1Body<true, true>, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else soa_cp_kernel<Pass1Body<true, false>, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        if (stats) soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<true, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<true, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
     } else {
-        if (stats) soa_cp_kernel<Pass1Body<false, true>, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else soa_cp_kernel<Pass1Body<false, false>, false><<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, {n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        if (stats) soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<false, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        else soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<false, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
     }
 }
 

@@ -66,16 +66,6 @@ __device__ __forceinline__ void samples20(const double* X, Samples& s) {
     const V3 v12 = vsub(n2, n1), v43 = vsub(n3, n4), v56 = vsub(n6, n5), v87 = vsub(n7, n8);
     const V3 v14 = vsub(n4, n1), v23 = vsub(n3, n2), v58 = vsub(n8, n5), v67 = vsub(n7, n6);
     const V3 v15 = vsub(n5, n1), v26 = vsub(n6, n2), v48 = vsub(n8, n4), v37 = vsub(n7, n3);
-#ifdef HEXVAL_KEY_TREE
-    // balanced: per-vector max of 3, then a 3-ary tree over the 12 vectors
-    int m[12];
-    const V3* vs[12] = {&v12, &v43, &v56, &v87, &v14, &v23, &v58, &v67, &v15, &v26, &v48, &v37};
-#pragma unroll
-    for (int q = 0; q < 12; ++q) m[q] = max(abskey(vs[q]->x), max(abskey(vs[q]->y), abskey(vs[q]->z)));
-    const int m0 = max(m[0], max(m[1], m[2])), m1 = max(m[3], max(m[4], m[5]));
-    const int m2 = max(m[6], max(m[7], m[8])), m3 = max(m[9], max(m[10], m[11]));
-    s.ekey = max(max(m0, m1), max(m2, m3));
-#else
     int e = 0;
 #define HV_EK(v) e = max(e, max(abskey(v.x), max(abskey(v.y), abskey(v.z))))
     HV_EK(v12); HV_EK(v43); HV_EK(v56); HV_EK(v87);
@@ -83,7 +73,7 @@ __device__ __forceinline__ void samples20(const double* X, Samples& s) {
     HV_EK(v15); HV_EK(v26); HV_EK(v48); HV_EK(v37);
 #undef HV_EK
     s.ekey = e;
-#endif
+
     // corners: det(d_xi x, d_eta x, d_zeta x) with the 3 edges at the corner
     s.c[0] = det3(v12, v14, v15);
     s.c[1] = det3(v12, v23, v26);
