@@ -8,6 +8,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 import paper_1706_01613_b200 as hv
@@ -90,3 +91,18 @@ def test_product_path_never_touches_the_oracle():
             for bad in ("import paper_1706_01613_b200", "from paper_1706_01613_b200", "hexval_device",
                         "hexval.h", "import hexgen", "from hexgen"):
                 assert bad not in text, (f, bad)
+
+
+def test_binding_validation_without_gpu():
+    """The Python binding checks dtype, device and shape before any call (CPU tensors here)."""
+    torch = pytest.importorskip("torch")
+    with pytest.raises(ValueError):
+        hv.check_soa(torch.zeros((24, 4), dtype=torch.float64))           # not CUDA
+    with pytest.raises(TypeError):
+        hv.check_soa(torch.zeros((24, 4), dtype=torch.float32))           # wrong dtype
+    with pytest.raises(ValueError):
+        hv.check_indexed(torch.zeros((4, 3), dtype=torch.float64), torch.zeros((4, 8), dtype=torch.int64))
+    with pytest.raises(TypeError):
+        hv.check_soa([[0.0]])                                            # not a tensor
+    with pytest.raises(TypeError):
+        hv.check_soa_host(np.zeros((24, 3), np.float32), np.zeros(3, np.uint8))
