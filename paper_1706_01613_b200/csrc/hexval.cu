@@ -823,6 +823,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
     double* const sc = ws.coef + gw * 28 * K4_CAP;
     const unsigned total = *((volatile unsigned*)&ctl->n_sub);
     const unsigned n_exact = *((volatile unsigned*)&ctl->n_exact);
+    bool ex_left = n_exact > 0;                          // warp-uniform: the exact queue may hold items
     const unsigned lt_mask = (1u << lane) - 1u;
     if (lane <= MAX_DEPTH) W.cnt[lane] = 0;
     __syncwarp();
@@ -846,12 +847,13 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             // and at most as many are claimed as there are free slots), then hexes
             // pass 1 left undecided
             nb = 0;
-            while (nb < 32) {
+            while (ex_left && nb < 32) {
                 const unsigned want = 32u - (unsigned)nb;
                 unsigned eb = 0;
                 if (lane == 0) eb = atomicAdd(&ctl->ex_next, want);
                 eb = __shfl_sync(0xffffffffu, eb, 0);
                 const unsigned got = eb < n_exact ? min(want, n_exact - eb) : 0u;
+                ex_left = got == want;
                 if (got == 0) break;
                 bool sub = false;
                 uint32_t h = 0;
