@@ -371,33 +371,47 @@ def run_ours(args, world, rank, local):
         kern_us = {"error": str(exc)[:200]}
     p1_names = ("soa_cp_kernel", "idx_cp_kernel", "plain_kernel", "pass1_soa_wtma_kernel")
     p1_us = next((v for k, v in kern_us.items() if k in p1_names), None)
-    p1_us = dist_max(p1_us, world) if p1_us is not None else None
+    k4_us = kern_us.get("subdiv_kernel")
+    # every rank joins both reductions (-1: not measured on this rank)
+    p1_us = dist_max(p1_us if isinstance(p1_us, float) else -1.0, world)
+    k4_us = dist_max(k4_us if isinstance(k4_us, float) else -1.0, world)
+    p1_us = p1_us if p1_us > 0 else None
+    k4_us = k4_us if k4_us > 0 else None
     per = {k: v["ms"] / max(1, v["launches"]) for k, v in phases.items()}
     pass1_ms = dist_max(per["pass1"], world)
     subdiv_ms = dist_max(per["subdiv"], world)
+    if k4_us is not None:
+        subdiv_ms = k4_us * 1e-3                                       # CUPTI kernel duration (see roofline.timing)
 
     value = world * n / (ms_step * 1e-3)
     peak, peak_src = measured_peaks()
     algo = algorithmic_bytes(layout, n, host, args.coeffs)
-    achieved = algo / (pass1_ms * 1e-3) / 1e9
+    achieved_ev = algo / (pass1_ms * 1e-3) / 1e9
+    # the kernel's own duration: CUPTI activity records when available (an event
+    # pair around a single kernel adds a launch bubble of 10-40 us here, see
+    # profiles/r01/SUMMARY.md "Event bubbles"), else the event pair
+    p1_s = p1_us * 1e-6 if p1_us else pass1_ms * 1e-3
+    achieved = algo / p1_s / 1e9
     traffic = ncu_traffic()
     roofline = {
-        "bound": "hbm", "kernel": "pass1 (K1 SoA warp-TMA staged / K2 indexed gather)",
+        "bound": "hbm", "kernel": "pass1 (K1 SoA cp.async double-buffered / K2 indexed cp.async gather)",
         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "duration_source": "cupti" if p1_us else "events",
+        "pass1_us": p1_s * 1e6,
+        "achieved_events": achieved_ev, "frac_events": achieved_ev / peak,
         "peak_source": peak_src,
         "algorithmic_bytes_per_launch": algo,
         "traffic": (traffic["dram_bytes_per_hex"] * n if traffic and cfg == 1 and not args.coeffs else None),
         "traffic_source": (traffic.get("source") if traffic and cfg == 1 and not args.coeffs else None),
         "frac_of_8TBs_nominal": achieved / 8000.0,
-        "pass1_ms": pass1_ms,
-        "pass1_share_of_step": pass1_ms / ms_step_prof,
-        "phase_ms_per_step": per,
-        "ms_per_step_profiled": ms_step_prof,
+        "pass1_share_of_step": p1_s * 1e3 / ms_step,
         "kernel_us_cupti": kern_us,
-        "achieved_cupti": (algo / (p1_us * 1e-6) / 1e9) if p1_us else None,
-        "frac_cupti": (algo / (p1_us * 1e-6) / 1e9 / peak) if p1_us else None,
-        "pass1_only_hex_per_s": n / (pass1_ms * 1e-3),
-        "timing": "CUDA events recorded by the library on the launching stream around each kernel, averaged over a second run of the K timed steps (ms_per_step_profiled is that run's step time)",
+        "phase_ms_per_step_events": per,
+        "ms_per_step_profiled": ms_step_prof,
+        "pass1_only_hex_per_s": n / p1_s,
+        "timing": ("pass1_us: mean kernel duration over min(K, 20) calls from CUPTI activity records (torch.profiler), "
+                   "live on the timed stream; *_events: CUDA events recorded by the library around each kernel over a "
+                   "second run of the K timed steps (ms_per_step_profiled is that run's step time)"),
     }
     subdivision = {
         "rate": st["n_subdivided"] / (world * n),
