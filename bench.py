@@ -65,6 +65,8 @@ def parse():
     p.add_argument("--config", type=int, default=1, choices=sorted(CONFIG_DESC))
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--graph", action="store_true",
+                   help="also time the call captured in a CUDA graph (launch-bound small batches)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
     p.add_argument("--coeffs", action="store_true",
@@ -350,6 +352,28 @@ def run_ours(args, world, rank, local):
         barrier(world)
     ms_total = ev0.elapsed_time(ev1)
     ms_step = dist_max(ms_total / args.steps, world)
+    graph = None
+    if args.graph:
+        # the same call captured once in a CUDA graph and replayed K times
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            step()
+        for _ in range(args.warmup):
+            g.replay()
+        barrier(world)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            g.replay()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        ms_g = dist_max(ev0.elapsed_time(ev1) / args.steps, world)
+        graph = {"ms_per_step": ms_g, "value": world * n / (ms_g * 1e-3),
+                 "timing": "torch.cuda.CUDAGraph of one call, K replays between two CUDA events"}
     # timed region 2: the same K steps with the library's per-kernel events
     # (hexval_profile) for the roofline and the phase split
     prof = hv.Profile()
@@ -357,14 +381,28 @@ def run_ours(args, world, rank, local):
     ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
     torch.cuda.synchronize()
-    ev2.record(stream)
-    for _ in range(args.steps):
-        step(profile=prof)
-    ev3.record(stream)
-    torch.cuda.synchronize()
+    phases = {}
+
+    def drain():                                                       # the profile holds 256 calls
+        for k, v in prof.read().items():
+            acc = phases.setdefault(k, {"ms": 0.0, "launches": 0})
+            acc["ms"] += v["ms"]
+            acc["launches"] += v["launches"]
+
+    ms_prof = 0.0
+    done = 0
+    while done < args.steps:
+        chunk = min(200, args.steps - done)
+        ev2.record(stream)
+        for _ in range(chunk):
+            step(profile=prof)
+        ev3.record(stream)
+        torch.cuda.synchronize()
+        ms_prof += ev2.elapsed_time(ev3)
+        drain()
+        done += chunk
     barrier(world)
-    ms_step_prof = dist_max(ev2.elapsed_time(ev3) / args.steps, world)
-    phases = prof.read()
+    ms_step_prof = dist_max(ms_prof / args.steps, world)
     try:
         kern_us = cupti_kernel_us(step, min(args.steps, 20))
     except Exception as exc:                                          # profiler unavailable: report without it
@@ -474,6 +512,7 @@ def run_ours(args, world, rank, local):
             "gpu_launches": hv.kernel_launches_per_call() * args.steps,
             "clocks": clk.summary(),
             "subdivision": subdivision,
+            **({"graph": graph} if graph else {}),
             "subdivision_rate": st["n_subdivided"] / (world * n),
             "verdicts": {"valid": st["n_valid"], "invalid": st["n_invalid"],
                          "undetermined": st["n_undetermined"], "nonfinite": st["n_nonfinite"],

@@ -211,7 +211,11 @@ int hexval_check_indexed_host(const double* vertices_host, int64_t nv,
  * stream, hexval_profile_read() adds up the elapsed time of every recorded
  * phase since the last read into ms_out[HEXVAL_NUM_PHASES] and the launch
  * counts into launches_out[HEXVAL_NUM_PHASES] (either may be NULL), then
- * resets.  Returns HEXVAL_OK or HEXVAL_ERR_CUDA.                           */
+ * resets.  Returns HEXVAL_OK or HEXVAL_ERR_CUDA.  A profile records at most
+ * 256 calls between reads; a *_ex call with a full profile returns
+ * HEXVAL_ERR_ARGUMENT and launches nothing.  Each phase is bracketed by a CUDA
+ * event pair on the call's stream, which adds a launch bubble to the recorded
+ * time.                                          */
 hexval_profile* hexval_profile_create(void);
 void hexval_profile_destroy(hexval_profile* p);
 int hexval_profile_read(hexval_profile* p, double* ms_out, long long* launches_out);

@@ -2075,7 +2075,7 @@ int hexval_profile_read(hexval_profile* p, double* ms_out, long long* launches_o
 const char* hexval_status_string(int status) {
     switch (status) {
         case HEXVAL_OK: return "ok";
-        case HEXVAL_ERR_ARGUMENT: return "invalid argument (n < 0, n > INT32_MAX, or NULL buffer)";
+        case HEXVAL_ERR_ARGUMENT: return "invalid argument (n < 0, n > INT32_MAX, NULL buffer, or a profile holding 256 unread calls)";
         case HEXVAL_ERR_ALIGNMENT: return "misaligned pointer";
         case HEXVAL_ERR_CUDA: return "CUDA launch or copy error";
         case HEXVAL_ERR_ALLOC: return "scratch allocation failed";

@@ -109,6 +109,49 @@ def test_nonfinite_and_empty():
     assert fl.numel() == 0
 
 
+def test_cuda_graph_capture_and_replay():
+    """The call is stream-ordered end to end (scratch via cudaMallocAsync, no host
+    sync), so a caller can capture it in a CUDA graph and replay it on new data."""
+    n = 20011
+    a = hexgen.ragged_soa(n, seed=7, amp=0.45)
+    b = hexgen.ragged_soa(n, seed=8, amp=0.45)
+    ref_b = oracle.check_soa(b)
+    static_in = torch.from_numpy(a).cuda()
+    flags = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        hv.check_soa(static_in, flags=flags)                     # warm (device info, pool)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        hv.check_soa(static_in, flags=flags)
+    for _ in range(3):
+        static_in.copy_(torch.from_numpy(b))
+        g.replay()
+    torch.cuda.synchronize()
+    assert_flags_match(flags.cpu().numpy(), ref_b, allow_near=True)
+    static_in.copy_(torch.from_numpy(a))
+    g.replay()
+    torch.cuda.synchronize()
+    eager, _ = gpu_soa(a)
+    assert np.array_equal(flags.cpu().numpy(), eager)
+
+
+def test_side_stream_matches_default_stream():
+    coords = hexgen.ragged_soa(4099, seed=11, amp=0.45)
+    dev = torch.from_numpy(coords).cuda()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        f1, _ = hv.check_soa(dev)
+    f2, _ = hv.check_soa(dev, stream=s)
+    s.synchronize()
+    f0, _ = gpu_soa(coords)
+    assert np.array_equal(f1.cpu().numpy(), f0) and np.array_equal(f2.cpu().numpy(), f0)
+
+
 # --------------------------------------------------------------------------
 # small configs, ragged sizes, exact path, subdivision
 # --------------------------------------------------------------------------
