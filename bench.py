@@ -65,6 +65,8 @@ def parse():
     p.add_argument("--config", type=int, default=1, choices=sorted(CONFIG_DESC))
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cupti", action="store_true",
+                   help="skip the torch.profiler (CUPTI) kernel-duration pass (e.g. under ncu)")
     p.add_argument("--graph", action="store_true",
                    help="also time the call captured in a CUDA graph (launch-bound small batches)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -403,10 +405,13 @@ def run_ours(args, world, rank, local):
         done += chunk
     barrier(world)
     ms_step_prof = dist_max(ms_prof / args.steps, world)
-    try:
-        kern_us = cupti_kernel_us(step, min(args.steps, 20))
-    except Exception as exc:                                          # profiler unavailable: report without it
-        kern_us = {"error": str(exc)[:200]}
+    if args.no_cupti:
+        kern_us = {"skipped": "--no-cupti"}
+    else:
+        try:
+            kern_us = cupti_kernel_us(step, min(args.steps, 20))
+        except Exception as exc:                                      # profiler unavailable: report without it
+            kern_us = {"error": str(exc)[:200]}
     p1_names = ("soa_cp_kernel", "idx_cp_kernel", "plain_kernel", "pass1_soa_wtma_kernel")
     p1_us = next((v for k, v in kern_us.items() if k in p1_names), None)
     k4_us = kern_us.get("subdiv_kernel")

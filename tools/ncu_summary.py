@@ -4,6 +4,8 @@
 usage:
   python tools/ncu_summary.py launches <launches.csv>          per-kernel launch times and shares
   python tools/ncu_summary.py full <report.ncu-rep> [algo_bytes_per_launch]
+  python tools/ncu_summary.py traffic <report.ncu-rep> <n_hexes> <out.json>
+      DRAM bytes per hex of the first kernel in the capture (bench.py's roofline.traffic)
 """
 from __future__ import annotations
 
@@ -73,6 +75,23 @@ def launches(path: str) -> None:
         print(f"| `{k}` | {len(v)} | {sum(v) / len(v) / 1e3:.2f} | {sum(v) / 1e3:.1f} | {sum(v) / total:.1%} |")
 
 
+def traffic(path: str, n: int, out_json: str) -> None:
+    import json
+    import os
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, u, r = rows[0], rows[1], rows[2]
+    rd = to_bytes(r[h.index("dram__bytes_read.sum")], u[h.index("dram__bytes_read.sum")])
+    wr = to_bytes(r[h.index("dram__bytes_write.sum")], u[h.index("dram__bytes_write.sum")])
+    name = r[h.index("Kernel Name")].split("(")[0] if "Kernel Name" in h else "?"
+    rec = {"dram_bytes_per_hex": round((rd + wr) / n, 4),
+           "source": f"{os.path.relpath(path)}: dram__bytes_read.sum {rd / 1e9:.6f} GB + dram__bytes_write.sum "
+                     f"{wr / 1e6:.4f} MB for one {name} launch over {n} hexes"}
+    with open(out_json, "w") as fh:
+        json.dump(rec, fh)
+    print(json.dumps(rec))
+
+
 def full(path: str, algo: float | None) -> None:
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -97,5 +116,7 @@ def full(path: str, algo: float | None) -> None:
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "traffic":
+        traffic(sys.argv[2], int(sys.argv[3]), sys.argv[4])
     else:
         full(sys.argv[2], float(sys.argv[3]) if len(sys.argv) > 3 else None)
