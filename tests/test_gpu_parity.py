@@ -203,6 +203,23 @@ def test_misaligned_base_uses_plain_path_with_same_results():
     assert np.array_equal(f1.cpu().numpy(), f2) and np.array_equal(k1.cpu().numpy(), k2)
 
 
+@pytest.mark.parametrize("shift_idx,shift_verts", [(1, 0), (2, 1), (0, 1)])
+def test_indexed_misaligned_pointers_same_results(shift_idx, shift_verts):
+    """Connectivity 4-B (not 16-B) aligned takes the plain gather kernel; vertices
+    8-B (not 16-B) aligned stay on the pipelined one: same bits either way."""
+    verts, idx = hexgen.indexed_config(3, start=777, count=256 * 148 + 999)
+    ref_f, ref_k = gpu_indexed(verts, idx, coeffs=True)
+    bi = torch.empty(idx.size + shift_idx, dtype=torch.int32, device="cuda")
+    bi[shift_idx:] = torch.from_numpy(idx.ravel()).cuda()
+    bv = torch.empty(verts.size + shift_verts, dtype=torch.float64, device="cuda")
+    bv[shift_verts:] = torch.from_numpy(verts.ravel()).cuda()
+    iv = bi[shift_idx:].view(idx.shape)
+    vv = bv[shift_verts:].view(verts.shape)
+    f, k = hv.check_indexed(vv, iv, coeffs=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(f.cpu().numpy(), ref_f) and np.array_equal(k.cpu().numpy(), ref_k)
+
+
 def test_pass1_variants_bit_identical(tmp_path):
     """HEXVAL_PASS1=ldg|wtma|cp (tuning knob) give identical flags and coefficients."""
     import subprocess
