@@ -152,6 +152,34 @@ def test_side_stream_matches_default_stream():
     assert np.array_equal(f1.cpu().numpy(), f0) and np.array_equal(f2.cpu().numpy(), f0)
 
 
+def test_concurrent_calls_on_two_streams_and_threads():
+    """Scratch is per call and device setup is guarded, so calls from two host
+    threads on two streams (ctypes releases the GIL) give the single-call results."""
+    import threading
+    a = hexgen.ragged_soa(300_001, seed=21, amp=0.45)
+    b = hexgen.ragged_soa(200_003, seed=22, amp=0.45)
+    fa0, _ = gpu_soa(a)
+    fb0, _ = gpu_soa(b)
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    out = {}
+
+    def run(key, dev):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(5):
+                f, _ = hv.check_soa(dev, stream=s)
+        s.synchronize()
+        out[key] = f.cpu().numpy()
+
+    torch.cuda.synchronize()
+    ts = [threading.Thread(target=run, args=("a", da)), threading.Thread(target=run, args=("b", db))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert np.array_equal(out["a"], fa0) and np.array_equal(out["b"], fb0)
+
+
 # --------------------------------------------------------------------------
 # small configs, ragged sizes, exact path, subdivision
 # --------------------------------------------------------------------------
