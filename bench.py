@@ -179,7 +179,7 @@ def cupti_kernel_us(step, steps: int) -> dict:
         d = per.setdefault(key, [0, 0.0])
         d[0] += 1
         d[1] += ev.time_range.end - ev.time_range.start
-    return {k: tot / c for k, (c, tot) in per.items()}
+    return {k: tot / c for k, (c, tot) in per.items()}, {k: c for k, (c, _) in per.items()}
 
 
 def dist_setup(gpus: int):
@@ -409,7 +409,7 @@ def run_ours(args, world, rank, local):
         kern_us = {"skipped": "--no-cupti"}
     else:
         try:
-            kern_us = cupti_kernel_us(step, min(args.steps, 20))
+            kern_us, _ = cupti_kernel_us(step, min(args.steps, 20))
         except Exception as exc:                                      # profiler unavailable: report without it
             kern_us = {"error": str(exc)[:200]}
     p1_names = ("soa_cp_kernel", "idx_cp_kernel", "plain_kernel", "pass1_soa_wtma_kernel")
@@ -623,6 +623,14 @@ def run_op(args, world, rank, local):
         torch.cuda.synchronize()
         barrier(world)
     ms = dist_max(ev0.elapsed_time(ev1) / args.steps, world)
+    kern_us, launches = {}, None
+    if not args.no_cupti:
+        try:
+            ksteps = min(args.steps, 20)
+            kern_us, kcount = cupti_kernel_us(step, ksteps)
+            launches = sum(c for k, c in kcount.items() if not k.startswith("Memset")) // ksteps * args.steps
+        except Exception as exc:                                      # profiler unavailable
+            kern_us = {"error": str(exc)[:200]}
     if in_bytes is None:
         in_bytes = 192 * n if layout == "soa" else 32 * n + 24 * host[0].shape[0]
     algo = in_bytes + out_bytes * n + (4 * extra.get("n_valid", 0) if args.op == "select" else 0)
@@ -636,8 +644,10 @@ def run_op(args, world, rank, local):
                                     if args.op == "quads" else CONFIG_DESC[cfg]),
                        "layout": layout, "n_per_rank": n},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                         "peak_source": peak_src, "algorithmic_bytes_per_launch": algo},
-            "gpu_launches": args.steps, "clocks": clk.summary(), **extra}), flush=True)
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": algo,
+                         "kernel_us_cupti": kern_us},
+            "gpu_launches": launches if launches is not None else args.steps,
+            "clocks": clk.summary(), **extra}), flush=True)
     return 0
 
 

@@ -23,13 +23,13 @@ def main(paths):
             op = d.get("op", "check")
             cfg = (d.get("config") or {}).get("workload", "")[:40]
             notes = []
+            ph = r.get("kernel_us_cupti") or {}
+            if any(isinstance(v, float) for v in ph.values()):
+                notes.append("kernels us: " + ", ".join(f"{k} {v:.1f}" for k, v in ph.items() if isinstance(v, float)))
+            elif op == "check":
+                ph = r.get("phase_ms_per_step", {})
+                notes.append("phases us: " + ", ".join(f"{k} {v * 1e3:.1f}" for k, v in ph.items()))
             if op == "check":
-                ph = r.get("kernel_us_cupti") or {}
-                if ph:
-                    notes.append("kernels us: " + ", ".join(f"{k} {v:.1f}" for k, v in ph.items() if isinstance(v, float)))
-                else:
-                    ph = r.get("phase_ms_per_step", {})
-                    notes.append("phases us: " + ", ".join(f"{k} {v * 1e3:.1f}" for k, v in ph.items()))
                 sub = d.get("subdivision") or {}
                 if sub.get("nodes_per_s"):
                     notes.append(f"{sub['nodes_per_step']:.3g} nodes, {sub['nodes_per_s'] / 1e9:.2f} G nodes/s")
