@@ -73,7 +73,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
     p.add_argument("--coeffs", action="store_true",
                    help="also write the 27 Bezier coefficients per hex (409 B/hex, SURVEY.md 8(d))")
-    p.add_argument("--op", choices=["check", "quality", "bounds", "select", "quads"], default="check",
+    p.add_argument("--op", choices=["check", "quality", "screen", "bounds", "select", "quads"], default="check",
                    help="check: the hot path (headline); quality: NEXT-2 corner screening kernel; "
                         "bounds: NEXT-1 certified min det J bounds; select: NEXT-3 candidate filtering "
                         "(on the config's flags); quads: NEXT-4 linear quadrangles (10M, noise 0.35)")
@@ -579,6 +579,18 @@ def run_op(args, world, rank, local):
         out_bytes = 0
         extra_sel = {"n_valid": n_valid, "groups": groups}
         metric = "candidates filtered/sec (VALID ids + per-cell counts, 1 B200)"
+    elif args.op == "screen":
+        fl = torch.empty(n, dtype=torch.uint8, device="cuda")
+        sj = torch.empty(n, dtype=torch.float64, device="cuda")
+        t1 = torch.empty(n, dtype=torch.uint8, device="cuda")
+
+        def step():
+            if layout == "soa":
+                hv.check_screen_soa(dev[0], fl, sj, t1)
+            else:
+                hv.check_screen_indexed(dev[0], dev[1], fl, sj, t1)
+        out_bytes = 10
+        metric = "hexahedra validated + screened/sec (flags, corner scaled Jacobian, Test 1 in one pass, fp64, 1 B200)"
     elif args.op == "quality":
         sj = torch.empty(n, dtype=torch.float64, device="cuda")
         t1 = torch.empty(n, dtype=torch.uint8, device="cuda")

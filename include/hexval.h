@@ -140,6 +140,20 @@ int hexval_corner_quality_indexed(const double* vertices, const int32_t* hex_idx
                                   double* sj_min_out_opt, uint8_t* test1_out_opt,
                                   cudaStream_t stream);
 
+/* Validity and the screening outputs in ONE pass over the coordinates (SURVEY
+ * 8(f) NEXT-2 "fused screening outputs"): flags_out exactly as
+ * hexval_check_soa / hexval_check_indexed (section 6), and
+ * sj_min_out[i] / test1_out[i] exactly as hexval_corner_quality_* (bit-identical:
+ * the same corner samples and the same arithmetic), computed by the pass-1
+ * kernel from the corner samples it evaluates anyway.  All three outputs are
+ * required (device memory); no coefficient output.  Asynchronous on `stream`;
+ * returns HEXVAL_OK or a negative status.                                        */
+int hexval_check_screen_soa(const double* coords, int64_t n, uint8_t* flags_out,
+                            double* sj_min_out, uint8_t* test1_out, cudaStream_t stream);
+int hexval_check_screen_indexed(const double* vertices, const int32_t* hex_idx, int64_t n,
+                                uint8_t* flags_out, double* sj_min_out, uint8_t* test1_out,
+                                cudaStream_t stream);
+
 /* ---- NEXT-1: certified bounds on min det J ------------------------------------
  * For every hex: lower_out[i] <= min over [0,1]^3 of det J <= upper_out[i] (device
  * memory, n doubles each).  lower = min of the Bezier coefficients over the leaves of

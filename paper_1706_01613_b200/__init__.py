@@ -24,7 +24,7 @@ __all__ = [
     "HexvalError", "lib", "library_path", "check_soa", "check_indexed", "check_soa_host",
     "check_indexed_host", "classify_bezier", "Stats", "Profile", "status_string", "version",
     "kernel_launches_per_call", "corner_quality_soa", "corner_quality_indexed", "min_detj_bounds_soa",
-    "min_detj_bounds_indexed", "select_valid", "check_quad_soa",
+    "min_detj_bounds_indexed", "select_valid", "check_quad_soa", "check_screen_soa", "check_screen_indexed",
 ]
 
 INVALID, VALID, UNDETERMINED, NONFINITE = 0, 1, 2, 3
@@ -70,6 +70,10 @@ def _load() -> ctypes.CDLL:
     L.hexval_corner_quality_indexed.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp]
     L.hexval_corner_quality_soa.restype = ctypes.c_int
     L.hexval_corner_quality_indexed.restype = ctypes.c_int
+    L.hexval_check_screen_soa.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp]
+    L.hexval_check_screen_indexed.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp, _vp]
+    L.hexval_check_screen_soa.restype = ctypes.c_int
+    L.hexval_check_screen_indexed.restype = ctypes.c_int
     L.hexval_min_detj_bounds_soa.argtypes = [_vp, _i64, ctypes.c_double, _vp, _vp, _vp, _vp, _vp]
     L.hexval_min_detj_bounds_indexed.argtypes = [_vp, _vp, _i64, ctypes.c_double, _vp, _vp, _vp, _vp, _vp]
     L.hexval_min_detj_bounds_soa.restype = ctypes.c_int
@@ -343,6 +347,42 @@ def corner_quality_indexed(vertices, hex_idx, sj_min=None, test1=None, stream=No
                                                test1.data_ptr(), _stream_handle(stream)),
            "hexval_corner_quality_indexed")
     return sj_min, test1
+
+
+def check_screen_soa(coords, flags=None, sj_min=None, test1=None, stream=None):
+    """hexval_check_screen_soa: validity flags plus the NEXT-2 screening outputs in one pass.
+
+    Returns ``(flags, sj_min, test1)``, bit-identical to ``check_soa`` and ``corner_quality_soa``."""
+    torch = _torch()
+    _require(coords, torch.float64, "coords", 2)
+    if coords.shape[0] != 24:
+        raise ValueError("coords must have shape (24, n)")
+    n = coords.shape[1]
+    if flags is None:
+        flags = torch.empty(n, dtype=torch.uint8, device=coords.device)
+    _require(flags, torch.uint8, "flags")
+    sj_min, test1 = _quality_outputs(n, coords.device, sj_min, test1)
+    _check(lib().hexval_check_screen_soa(coords.data_ptr(), n, flags.data_ptr(), sj_min.data_ptr(),
+                                         test1.data_ptr(), _stream_handle(stream)), "hexval_check_screen_soa")
+    return flags, sj_min, test1
+
+
+def check_screen_indexed(vertices, hex_idx, flags=None, sj_min=None, test1=None, stream=None):
+    """hexval_check_screen_indexed: ``check_indexed`` and ``corner_quality_indexed`` in one pass."""
+    torch = _torch()
+    _require(vertices, torch.float64, "vertices", 2)
+    _require(hex_idx, torch.int32, "hex_idx", 2)
+    if vertices.shape[1] != 3 or hex_idx.shape[1] != 8:
+        raise ValueError("vertices must be (nv, 3) and hex_idx (n, 8)")
+    n = hex_idx.shape[0]
+    if flags is None:
+        flags = torch.empty(n, dtype=torch.uint8, device=hex_idx.device)
+    _require(flags, torch.uint8, "flags")
+    sj_min, test1 = _quality_outputs(n, hex_idx.device, sj_min, test1)
+    _check(lib().hexval_check_screen_indexed(vertices.data_ptr(), hex_idx.data_ptr(), n, flags.data_ptr(),
+                                             sj_min.data_ptr(), test1.data_ptr(), _stream_handle(stream)),
+           "hexval_check_screen_indexed")
+    return flags, sj_min, test1
 
 
 def _bounds_outputs(n, device, lower, upper, status):

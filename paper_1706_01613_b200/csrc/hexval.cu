@@ -263,17 +263,53 @@ __device__ __forceinline__ void warp_epilogue(int st, int64_t i, Ctl* ctl, uint3
 // ---------------------------------------------------------------------------
 // K1 / K2: pass 1
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ double len2(const V3& v) {
+    return __fma_rn(v.z, v.z, __fma_rn(v.y, v.y, __dmul_rn(v.x, v.x)));
+}
+
+// NEXT-2 per hex from the 12 edge vectors E (samples20 order) and the 8 corner
+// samples c: Test 1 (all c > 0) and the minimum corner scaled Jacobian
+// c / (|d_xi x||d_eta x||d_zeta x|), the argmin taken by
+// cross-multiplication so only the winner pays a division and a sqrt.  Shared
+// by quality_kernel and the fused pass 1 (bit-identical outputs).
+__device__ __forceinline__ void corner_quality(const V3* E, const double* c, double& sj, uint8_t& t1) {
+    const double l12 = len2(E[0]), l43 = len2(E[1]), l56 = len2(E[2]), l87 = len2(E[3]);
+    const double l14 = len2(E[4]), l23 = len2(E[5]), l58 = len2(E[6]), l67 = len2(E[7]);
+    const double l15 = len2(E[8]), l26 = len2(E[9]), l48 = len2(E[10]), l37 = len2(E[11]);
+    const double P[8] = {__dmul_rn(__dmul_rn(l12, l14), l15), __dmul_rn(__dmul_rn(l12, l23), l26),
+                         __dmul_rn(__dmul_rn(l43, l23), l37), __dmul_rn(__dmul_rn(l43, l14), l48),
+                         __dmul_rn(__dmul_rn(l56, l58), l15), __dmul_rn(__dmul_rn(l56, l67), l26),
+                         __dmul_rn(__dmul_rn(l87, l67), l37), __dmul_rn(__dmul_rn(l87, l58), l48)};
+    int km = key(c[0]);
+    double bn = __dmul_rn(c[0], fabs(c[0])), bp = P[0];
+    bool zero_edge = !(P[0] > 0.0);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+        km = min(km, key(c[k]));
+        zero_edge |= !(P[k] > 0.0);
+        const double nk = __dmul_rn(c[k], fabs(c[k]));
+        if (__dmul_rn(nk, bp) < __dmul_rn(bn, P[k])) { bn = nk; bp = P[k]; }   // nk/P[k] < bn/bp
+    }
+    t1 = km > 0;
+    sj = zero_edge ? __longlong_as_double(0x7ff8000000000000ll) : copysign(sqrt(__ddiv_rn(fabs(bn), bp)), bn);
+}
+
 // S1-S5 + S8 for one hex whose 24 coordinates are in registers; returns the
 // pass-1 state (ST_*).
-template <bool COEFFS, class L>
+// QUAL: also the fused NEXT-2 screening outputs (corner_quality) of the hex.
+template <bool COEFFS, class L, bool QUAL = false>
 __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i, int64_t n,
-                                         uint8_t* __restrict__ flags, double* __restrict__ coeffs) {
+                                         uint8_t* __restrict__ flags, double* __restrict__ coeffs,
+                                         double* __restrict__ sj_out = nullptr, uint8_t* __restrict__ t1_out = nullptr) {
     int st;
+    double sj = __longlong_as_double(0x7ff8000000000000ll);
+    uint8_t t1 = 0;
     if (out_of_range(X)) {
         st = ST_NONFINITE;
     } else {
         Samples s;
-        samples20(X, s);                                  // S1 + S2
+        if (QUAL) samples20(X, s, [&](const V3* E, const double* c) { corner_quality(E, c, sj, t1); });
+        else samples20(X, s);                             // S1 + S2
         st = step2_class<L::kIntStep2>(s, step2_tau(s.ekey));   // S3 (Step 2)
         if (st == ST_EXACT && ld.dup_face_pair(i)) st = ST_INVALID;   // a sample is exactly 0
         Coeffs t;
@@ -290,6 +326,10 @@ __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i
         default: f = PENDING_EXACT; break;
     }
     __stcs(flags + i, f);
+    if (QUAL) {
+        __stcs(sj_out + i, sj);
+        __stcs(t1_out + i, t1);
+    }
     return st;
 }
 
@@ -459,8 +499,8 @@ __device__ __forceinline__ void cp_issue_hex(const double* __restrict__ coords, 
 // Per-hex bodies run by the pipelines below.  hex() runs on the lanes that
 // own a hex (X in registers) and returns a state; epilogue() is warp-collective
 // (every lane, st = -1 without a hex); finish() once per thread at the end.
-template <bool COEFFS, bool STATS>
-struct Pass1Body {                                           // K1/K2: S1-S8 + K3
+template <bool COEFFS, bool STATS, bool QUAL = false>
+struct Pass1Body {                                           // K1/K2: S1-S8 + K3 (+ NEXT-2 outputs)
     int64_t n;
     uint8_t* flags;
     double* coeffs;
@@ -468,10 +508,12 @@ struct Pass1Body {                                           // K1/K2: S1-S8 + K
     uint32_t* qsub;
     uint32_t* qexact;
     hexval_stats* stats;
+    double* sj;
+    uint8_t* t1;
     P1Counts cnt;
     template <class L>
     __device__ __forceinline__ int hex(const L& ld, const double* X, int64_t i) {
-        return pass1_hex<COEFFS>(ld, X, i, n, flags, coeffs);
+        return pass1_hex<COEFFS, L, QUAL>(ld, X, i, n, flags, coeffs, sj, t1);
     }
     __device__ __forceinline__ void epilogue(int st, int64_t i) {
         warp_epilogue<false>(st, i, ctl, qsub, qexact, stats);
@@ -605,9 +647,6 @@ __global__ void __launch_bounds__(CP_THREADS, 2)
 // over the corners compares c|c|/P by cross-multiplication (P = product of the
 // squared edge lengths), so only the winner takes a division and a sqrt.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double len2(const V3& v) {
-    return __fma_rn(v.z, v.z, __fma_rn(v.y, v.y, __dmul_rn(v.x, v.x)));
-}
 
 template <class L>
 __global__ void __launch_bounds__(256) quality_kernel(L ld, int64_t n, double* __restrict__ sj_out,
@@ -627,25 +666,8 @@ __global__ void __launch_bounds__(256) quality_kernel(L ld, int64_t n, double* _
         // corner k: (d_xi, d_eta, d_zeta) = the three edges leaving it
         const double c[8] = {det3(v12, v14, v15), det3(v12, v23, v26), det3(v43, v23, v37), det3(v43, v14, v48),
                              det3(v56, v58, v15), det3(v56, v67, v26), det3(v87, v67, v37), det3(v87, v58, v48)};
-        const double l12 = len2(v12), l43 = len2(v43), l56 = len2(v56), l87 = len2(v87);
-        const double l14 = len2(v14), l23 = len2(v23), l58 = len2(v58), l67 = len2(v67);
-        const double l15 = len2(v15), l26 = len2(v26), l48 = len2(v48), l37 = len2(v37);
-        const double P[8] = {__dmul_rn(__dmul_rn(l12, l14), l15), __dmul_rn(__dmul_rn(l12, l23), l26),
-                             __dmul_rn(__dmul_rn(l43, l23), l37), __dmul_rn(__dmul_rn(l43, l14), l48),
-                             __dmul_rn(__dmul_rn(l56, l58), l15), __dmul_rn(__dmul_rn(l56, l67), l26),
-                             __dmul_rn(__dmul_rn(l87, l67), l37), __dmul_rn(__dmul_rn(l87, l58), l48)};
-        int km = key(c[0]);
-        double bn = __dmul_rn(c[0], fabs(c[0])), bp = P[0];
-        bool zero_edge = !(P[0] > 0.0);
-#pragma unroll
-        for (int k = 1; k < 8; ++k) {
-            km = min(km, key(c[k]));
-            zero_edge |= !(P[k] > 0.0);
-            const double nk = __dmul_rn(c[k], fabs(c[k]));
-            if (__dmul_rn(nk, bp) < __dmul_rn(bn, P[k])) { bn = nk; bp = P[k]; }   // nk/P[k] < bn/bp
-        }
-        t1 = km > 0;
-        if (!zero_edge) sj = copysign(sqrt(__ddiv_rn(fabs(bn), bp)), bn);
+        const V3 E[12] = {v12, v43, v56, v87, v14, v23, v58, v67, v15, v26, v48, v37};
+        corner_quality(E, c, sj, t1);
     }
     if (sj_out) __stcs(sj_out + i, sj);
     if (t1_out) __stcs(t1_out + i, t1);
@@ -1467,7 +1489,9 @@ bool cp_attr(size_t smem_soa, size_t smem_idx) {
 
 int cp_setup() {
     const bool ok = cp_attr<Pass1Body<false, false>>(CP_SMEM, CPI_SMEM) && cp_attr<Pass1Body<false, true>>(CP_SMEM, CPI_SMEM) &&
-                    cp_attr<Pass1Body<true, false>>(CP_SMEM, CPI_SMEM) && cp_attr<Pass1Body<true, true>>(CP_SMEM, CPI_SMEM);
+                    cp_attr<Pass1Body<true, false>>(CP_SMEM, CPI_SMEM) && cp_attr<Pass1Body<true, true>>(CP_SMEM, CPI_SMEM) &&
+                    cp_attr<Pass1Body<false, false, true>>(CP_SMEM, CPI_SMEM) &&
+                    cp_attr<Pass1Body<false, true, true>>(CP_SMEM, CPI_SMEM);
     if (!ok) {
         cudaGetLastError();
         return 0;
@@ -1529,86 +1553,89 @@ struct hexval_profile {
 
 namespace {
 
-template <class L>
-void launch_pass1_plain(const L& ld, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl, uint32_t* qsub,
-                        uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
-    const unsigned blocks = (unsigned)((n + P1_THREADS - 1) / P1_THREADS);
-    if (coeffs) {
-        if (stats) plain_kernel<<<blocks, P1_THREADS, 0, stream>>>(ld, n, Pass1Body<true, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else plain_kernel<<<blocks, P1_THREADS, 0, stream>>>(ld, n, Pass1Body<true, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+// The pass-1 body of a call: (coefficients, stats, fused screening outputs).
+struct P1Args {
+    int64_t n;
+    uint8_t* flags;
+    double* coeffs;
+    Ctl* ctl;
+    uint32_t* qsub;
+    uint32_t* qex;
+    hexval_stats* stats;
+    double* sj;                   // fused NEXT-2 outputs (both set or both null)
+    uint8_t* t1;
+};
+
+template <class F>
+void with_pass1_body(const P1Args& a, F&& f) {
+    if (a.sj) {
+        if (a.stats) f(Pass1Body<false, true, true>{a.n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats, a.sj, a.t1, {}});
+        else f(Pass1Body<false, false, true>{a.n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats, a.sj, a.t1, {}});
+    } else if (a.coeffs) {
+        if (a.stats) f(Pass1Body<true, true>{a.n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats, nullptr, nullptr, {}});
+        else f(Pass1Body<true, false>{a.n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats, nullptr, nullptr, {}});
     } else {
-        if (stats) plain_kernel<<<blocks, P1_THREADS, 0, stream>>>(ld, n, Pass1Body<false, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else plain_kernel<<<blocks, P1_THREADS, 0, stream>>>(ld, n, Pass1Body<false, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
+        if (a.stats) f(Pass1Body<false, true>{a.n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats, nullptr, nullptr, {}});
+        else f(Pass1Body<false, false>{a.n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats, nullptr, nullptr, {}});
     }
 }
 
 template <class L>
-void launch_pass1(const L& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl,
-                  uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream);
+void launch_pass1_plain(const L& ld, const P1Args& a, cudaStream_t stream) {
+    const unsigned blocks = (unsigned)((a.n + P1_THREADS - 1) / P1_THREADS);
+    with_pass1_body(a, [&](auto body) { plain_kernel<<<blocks, P1_THREADS, 0, stream>>>(ld, a.n, body); });
+}
+
+template <class L>
+void launch_pass1(const L& ld, const DeviceInfo& info, const P1Args& a, cudaStream_t stream);
 
 // indexed: the cp.async gather pipeline when the connectivity rows are 16-B
 // aligned (int4 loads), else the plain kernel
 template <>
-void launch_pass1<IdxLoader>(const IdxLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs,
-                             Ctl* ctl, uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
+void launch_pass1<IdxLoader>(const IdxLoader& ld, const DeviceInfo& info, const P1Args& a, cudaStream_t stream) {
     if (info.p1_variant != P1_CP || (((uintptr_t)ld.idx) & 15) != 0) {
-        launch_pass1_plain(ld, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+        launch_pass1_plain(ld, a, stream);
         return;
     }
-    const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
+    const int64_t tiles = (a.n + CP_THREADS - 1) / CP_THREADS;
     const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-    const double* v = ld.verts;
-    const int32_t* x = ld.idx;
-    if (coeffs) {
-        if (stats) idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, Pass1Body<true, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, Pass1Body<true, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-    } else {
-        if (stats) idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, Pass1Body<false, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(v, x, n, Pass1Body<false, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-    }
+    with_pass1_body(a, [&](auto body) {
+        idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(ld.verts, ld.idx, a.n, body);
+    });
 }
 
-void launch_wtma(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl,
-                 uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
-    const int64_t chunks = (n + 31) / 32;
+void launch_wtma(const SoaLoader& ld, const DeviceInfo& info, const P1Args& a, cudaStream_t stream) {
+    const int64_t chunks = (a.n + 31) / 32;
     const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
     const int64_t want = (chunks + WT_WARPS - 1) / WT_WARPS;
     const unsigned grid = (unsigned)(want < cap ? want : cap);
     const double* c = ld.coords;
-    if (coeffs) {
-        if (stats) pass1_soa_wtma_kernel<true, true><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_soa_wtma_kernel<true, false><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+    const int64_t n = a.n;
+    if (a.coeffs) {
+        if (a.stats) pass1_soa_wtma_kernel<true, true><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats);
+        else pass1_soa_wtma_kernel<true, false><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats);
     } else {
-        if (stats) pass1_soa_wtma_kernel<false, true><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
-        else pass1_soa_wtma_kernel<false, false><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, flags, coeffs, ctl, qsub, qex, stats);
+        if (a.stats) pass1_soa_wtma_kernel<false, true><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats);
+        else pass1_soa_wtma_kernel<false, false><<<grid, WT_THREADS, WT_SMEM, stream>>>(c, n, a.flags, a.coeffs, a.ctl, a.qsub, a.qex, a.stats);
     }
 }
 
-void launch_cp(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags, double* coeffs, Ctl* ctl,
-               uint32_t* qsub, uint32_t* qex, hexval_stats* stats, cudaStream_t stream) {
-    const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
+void launch_cp(const SoaLoader& ld, const DeviceInfo& info, const P1Args& a, cudaStream_t stream) {
+    const int64_t tiles = (a.n + CP_THREADS - 1) / CP_THREADS;
     const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
     const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-    const double* c = ld.coords;
-    if (coeffs) {
-        if (stats) soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<true, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<true, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-    } else {
-        if (stats) soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<false, true>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-        else soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(c, n, Pass1Body<false, false>{n, flags, coeffs, ctl, qsub, qex, stats, {}});
-    }
+    with_pass1_body(a, [&](auto body) { soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(ld.coords, a.n, body); });
 }
 
-// SoA: the selected variant (warp-TMA needs a 16-B aligned coordinate array).
+// SoA: the selected variant (warp-TMA needs a 16-B aligned coordinate array
+// and has no fused screening outputs).
 template <>
-void launch_pass1<SoaLoader>(const SoaLoader& ld, const DeviceInfo& info, int64_t n, uint8_t* flags,
-                             double* coeffs, Ctl* ctl, uint32_t* qsub, uint32_t* qex, hexval_stats* stats,
-                             cudaStream_t stream) {
+void launch_pass1<SoaLoader>(const SoaLoader& ld, const DeviceInfo& info, const P1Args& a, cudaStream_t stream) {
     const bool aligned = (((uintptr_t)ld.coords) & 15) == 0;
-    if (aligned && info.p1_variant == P1_WTMA) launch_wtma(ld, info, n, flags, coeffs, ctl, qsub, qex, stats, stream);
-    else if (info.p1_variant == P1_CP) launch_cp(ld, info, n, flags, coeffs, ctl, qsub, qex, stats, stream);
-    else launch_pass1_plain(ld, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+    if (aligned && info.p1_variant == P1_WTMA && !a.sj) launch_wtma(ld, info, a, stream);
+    else if (info.p1_variant == P1_CP) launch_cp(ld, info, a, stream);
+    else launch_pass1_plain(ld, a, stream);
 }
 
 template <class R>
@@ -1643,7 +1670,7 @@ int collect_profile(hexval_profile* p) {
 
 template <class L>
 int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_stats* stats,
-               hexval_profile* prof, cudaStream_t stream) {
+               hexval_profile* prof, cudaStream_t stream, double* sj = nullptr, uint8_t* t1 = nullptr) {
     if (n == 0) return HEXVAL_OK;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return HEXVAL_ERR_CUDA;
@@ -1674,7 +1701,7 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     };
 
     mark(HEXVAL_PHASE_PASS1, 0);
-    launch_pass1(ld, info, n, flags, coeffs, ctl, qsub, qex, stats, stream);
+    launch_pass1(ld, info, P1Args{n, flags, coeffs, ctl, qsub, qex, stats, sj, t1}, stream);
     mark(HEXVAL_PHASE_PASS1, 1);
     // K5 (exact signs) is fused into K4's batch filling: no separate launch
     mark(HEXVAL_PHASE_SUBDIV, 0);
@@ -1821,6 +1848,24 @@ int hexval_classify_bezier(const double* coeffs, int64_t n, uint8_t* flags_out, 
     if (n > 0 && (!coeffs || !flags_out)) return HEXVAL_ERR_ARGUMENT;
     if (misaligned(coeffs, 8) || misaligned(stats_dev_opt, 8)) return HEXVAL_ERR_ALIGNMENT;
     return run_bezier(coeffs, n, flags_out, stats_dev_opt, stream);
+}
+
+int hexval_check_screen_soa(const double* coords, int64_t n, uint8_t* flags_out, double* sj_min_out,
+                            uint8_t* test1_out, cudaStream_t stream) {
+    if (n < 0 || n > INT32_MAX) return HEXVAL_ERR_ARGUMENT;
+    if (n > 0 && (!coords || !flags_out || !sj_min_out || !test1_out)) return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(coords, 8) || misaligned(sj_min_out, 8)) return HEXVAL_ERR_ALIGNMENT;
+    SoaLoader ld{coords, n};
+    return run_device(ld, n, flags_out, nullptr, nullptr, nullptr, stream, sj_min_out, test1_out);
+}
+
+int hexval_check_screen_indexed(const double* vertices, const int32_t* hex_idx, int64_t n, uint8_t* flags_out,
+                                double* sj_min_out, uint8_t* test1_out, cudaStream_t stream) {
+    if (n < 0 || n > INT32_MAX) return HEXVAL_ERR_ARGUMENT;
+    if (n > 0 && (!vertices || !hex_idx || !flags_out || !sj_min_out || !test1_out)) return HEXVAL_ERR_ARGUMENT;
+    if (misaligned(vertices, 8) || misaligned(hex_idx, 4) || misaligned(sj_min_out, 8)) return HEXVAL_ERR_ALIGNMENT;
+    IdxLoader ld{vertices, hex_idx};
+    return run_device(ld, n, flags_out, nullptr, nullptr, nullptr, stream, sj_min_out, test1_out);
 }
 
 int hexval_corner_quality_soa(const double* coords, int64_t n, double* sj_min_out_opt, uint8_t* test1_out_opt,

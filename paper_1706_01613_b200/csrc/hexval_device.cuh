@@ -59,7 +59,15 @@ struct Samples {
     int ekey;        // abskey of max |edge component|
 };
 
-__device__ __forceinline__ void samples20(const double* X, Samples& s) {
+struct NoCornerHook {
+    __device__ __forceinline__ void operator()(const V3*, const double*) const {}
+};
+
+// corner(E, c): optional consumer of the 12 edge vectors E = {v12, v43, v56,
+// v87, v14, v23, v58, v67, v15, v26, v48, v37} and the 8 corner samples c,
+// called once they exist (the fused NEXT-2 screening outputs).
+template <class CornerHook = NoCornerHook>
+__device__ __forceinline__ void samples20(const double* X, Samples& s, CornerHook&& corner = CornerHook()) {
     const V3 n1{X[0], X[1], X[2]}, n2{X[3], X[4], X[5]}, n3{X[6], X[7], X[8]}, n4{X[9], X[10], X[11]};
     const V3 n5{X[12], X[13], X[14]}, n6{X[15], X[16], X[17]}, n7{X[18], X[19], X[20]}, n8{X[21], X[22], X[23]};
     // edge vectors v_ij = n_j - n_i
@@ -83,6 +91,10 @@ __device__ __forceinline__ void samples20(const double* X, Samples& s) {
     s.c[5] = det3(v56, v67, v26);
     s.c[6] = det3(v87, v67, v37);
     s.c[7] = det3(v87, v58, v48);
+    {
+        const V3 E[12] = {v12, v43, v56, v87, v14, v23, v58, v67, v15, v26, v48, v37};
+        corner(E, s.c);
+    }
     // twice the mid-edge derivatives (each shared by two edges)
     const V3 Se0 = vadd(v14, v23), Se1 = vadd(v58, v67);   // d_eta  at xi=1/2, zeta=0/1
     const V3 Sz0 = vadd(v15, v26), Sz1 = vadd(v48, v37);   // d_zeta at xi=1/2, eta=0/1

@@ -508,6 +508,42 @@ def test_corner_quality_special_cases(golden_hexes):
     _quality_parity(coords, sj, t1)
 
 
+@pytest.mark.parametrize("n", [1, 255, 257, 256 * 148 * 2 + 77])
+def test_fused_screen_equals_separate_calls(n):
+    """hexval_check_screen_soa: flags bit-identical to check_soa, sj/test1 bit-identical to
+    corner_quality_soa (same corner samples, same arithmetic), NaN/NONFINITE rows included."""
+    coords = hexgen.ragged_soa(n, seed=900 + n % 97, amp=0.45)
+    if n > 300:
+        coords[7, 5] = np.nan
+        coords[0, 6:9] = coords[3, 6:9]                         # nodes 1 and 2 coincide: zero edge
+        coords[1, 6:9] = coords[4, 6:9]
+        coords[2, 6:9] = coords[5, 6:9]
+    dev = torch.from_numpy(coords).cuda()
+    f, sj, t1 = hv.check_screen_soa(dev)
+    f0, _ = hv.check_soa(dev)
+    sj0, t10 = hv.corner_quality_soa(dev)
+    torch.cuda.synchronize()
+    assert np.array_equal(f.cpu().numpy(), f0.cpu().numpy())
+    a, b = sj.cpu().numpy(), sj0.cpu().numpy()
+    assert np.array_equal(np.isnan(a), np.isnan(b)) and np.array_equal(a[~np.isnan(a)], b[~np.isnan(b)])
+    assert np.array_equal(t1.cpu().numpy(), t10.cpu().numpy())
+    ref = oracle.check_soa(coords)
+    assert_flags_match(f.cpu().numpy(), ref, allow_near=True)
+
+
+def test_fused_screen_indexed_config3_slice():
+    verts, idx = hexgen.indexed_config(3, start=4242, count=256 * 148 + 555)
+    v, i = torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda()
+    f, sj, t1 = hv.check_screen_indexed(v, i)
+    f0, _ = hv.check_indexed(v, i)
+    sj0, t10 = hv.corner_quality_indexed(v, i)
+    torch.cuda.synchronize()
+    assert np.array_equal(f.cpu().numpy(), f0.cpu().numpy())
+    a, b = sj.cpu().numpy(), sj0.cpu().numpy()
+    assert np.array_equal(np.isnan(a), np.isnan(b)) and np.array_equal(a[~np.isnan(a)], b[~np.isnan(b)])
+    assert np.array_equal(t1.cpu().numpy(), t10.cpu().numpy())
+
+
 def test_corner_quality_indexed_config3_slice():
     verts, idx = hexgen.indexed_config(3, start=777, count=50_000)
     sj, t1 = hv.corner_quality_indexed(torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda())
