@@ -2128,7 +2128,7 @@ const char* hexval_status_string(int status) {
     }
 }
 
-int hexval_version(void) { return 110; }
+int hexval_version(void) { return 120; }
 
 int hexval_kernel_launches_per_call(void) { return 2; }
 
