@@ -490,8 +490,23 @@ def run_ours(args, world, rank, local):
         dt = time.perf_counter() - t0
         dt = dist_max(dt, world)
         h2d = sum(a.nbytes for a in host)
+        # the link's own ceiling: best of 3 plain pinned -> device copies of the largest input array
+        big = pins_[0]
+        dst = torch.empty(big.shape, dtype=big.dtype, device="cuda")
+        link = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dst.copy_(big, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            link = max(link, big.numel() * big.element_size() / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        del dst
         e2e = {"value": world * n * args.e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": n,
+               "h2d_gbs_achieved": h2d * args.e2e_steps / dt / 1e9,
+               "h2d_gbs_link": link,
+               "frac_of_link": (h2d * args.e2e_steps / dt / 1e9) / link if link else None,
                "timing": "host wall clock around the synchronous hexval_check_*_host call (H2D of pinned inputs, kernels, D2H of flags), max over ranks",
                "steps": args.e2e_steps}
         if not torch.equal(flags.cpu(), fl_h):
