@@ -1,11 +1,16 @@
 // hexval.cu -- kernels and C ABI of the B200 hot path for the robust validity
 // check of linear hexahedra (section 6).
 //
-//   K1/K2 pass1_kernel   one hex per thread: coalesced fp64 loads (SoA planes,
-//                        or int32 connectivity + vertex gather), 20 tet
-//                        determinants, Step 2, 27 Bezier coefficients, Step 4,
-//                        flags, optional coefficients, and (K3) warp-ballot +
-//                        block-scan compaction of undecided / ambiguous hexes.
+//   K1/K2 pass 1         one hex per thread (Pass1Body): 20 tet determinants,
+//                        Step 2, 27 Bezier coefficients, Step 4, flags,
+//                        optional coefficients / fused NEXT-2 screening
+//                        outputs, and (K3) warp-aggregated compaction of
+//                        undecided / ambiguous hexes.  Pipelines:
+//                        soa_cp_kernel (SoA planes, per-thread cp.async double
+//                        buffering), idx_cp_kernel (int32 connectivity, rows
+//                        and vertex gathers by cp.async, three deep),
+//                        plain_kernel (unaligned inputs; HEXVAL_PASS1=ldg) and
+//                        pass1_soa_wtma_kernel (per-warp TMA; A/B variant).
 //   K5    exact path     exact signs of root samples within their rounding
 //                        bound of 0 (Kulisch accumulator), then Steps 3-4;
 //                        drained by K4 while it fills its batches.
@@ -13,6 +18,9 @@
 //                        hexes and splits up to 32 same-depth nodes per step
 //                        (one per lane), children pushed on a per-warp
 //                        depth-sorted stack in global memory.
+//   NEXT rows            bounds_kernel (NEXT-1, K4's machinery with a bounds
+//                        policy), quality_kernel (NEXT-2), select_* (NEXT-3),
+//                        quad_kernel (NEXT-4).
 //
 // All launches go on the caller's stream; queue lengths are read on the
 // device, so there is no host synchronisation inside a call.
