@@ -4,8 +4,8 @@ set -u
 mkdir -p gpurun_out/final
 O=gpurun_out/final
 nvidia-smi > $O/nvidia_smi.txt 2>&1; (nproc; grep -m1 "model name" /proc/cpuinfo) > $O/host.txt
-timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 1800 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
 timeout 900 python bench.py > $O/bench.log 2>&1
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.log 2>&1
 for c in 2 3 4; do timeout 900 python bench.py --config $c --steps $([ $c = 4 ] && echo 3 || echo 20) --no-e2e > $O/bench_c$c.log 2>&1; done
