@@ -104,5 +104,9 @@ def test_binding_validation_without_gpu():
         hv.check_indexed(torch.zeros((4, 3), dtype=torch.float64), torch.zeros((4, 8), dtype=torch.int64))
     with pytest.raises(TypeError):
         hv.check_soa([[0.0]])                                            # not a tensor
+    with pytest.raises(ValueError):
+        hv.check_screen_soa(torch.zeros((24, 4), dtype=torch.float64))    # not CUDA
+    with pytest.raises(ValueError):
+        hv.check_screen_indexed(torch.zeros((4, 3), dtype=torch.float64), torch.zeros((4, 8), dtype=torch.int32))
     with pytest.raises(TypeError):
         hv.check_soa_host(np.zeros((24, 3), np.float32), np.zeros(3, np.uint8))
