@@ -31,8 +31,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
-
 METRIC = "hexahedra validated/sec (fp64, 1 B200); % of HBM roofline; subdivision rate"
 UNIT = "hex/s"
 FALLBACK_HBM_GBS = 6650.0
