@@ -531,6 +531,24 @@ def test_fused_screen_equals_separate_calls(n):
     assert_flags_match(f.cpu().numpy(), ref, allow_near=True)
 
 
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_test1_is_necessary_at_full_size(cfg):
+    """Ushakova's Test 1 is necessary for validity: over the whole
+    config, no hex the robust check calls VALID fails Test 1 (a property that holds at
+    any size, checked on every hex through the fused screening call)."""
+    if cfg == 1:
+        _, coords = hexgen.make(1)
+        f, sj, t1 = hv.check_screen_soa(torch.from_numpy(coords).cuda())
+    else:
+        verts, idx = hexgen.indexed_config(3)
+        f, sj, t1 = hv.check_screen_indexed(torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda())
+    torch.cuda.synchronize()
+    valid = (f & 3) == hv.VALID
+    assert int(valid.sum().item()) > 0
+    assert bool((t1[valid] == 1).all().item())
+    assert bool((sj[valid] > 0).all().item())
+
+
 def test_fused_screen_indexed_config3_slice():
     verts, idx = hexgen.indexed_config(3, start=4242, count=256 * 148 + 555)
     v, i = torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda()

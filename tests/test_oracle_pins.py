@@ -191,6 +191,21 @@ def test_subdivision_is_exact_reparameterisation():
             assert np.max(np.abs(pins.bezier_eval(child, loc) - pins.bezier_eval(b, glob))) <= 1e-14 * np.max(np.abs(b))
 
 
+def test_subdivision_children_lie_in_the_parent_hull():
+    """De Casteljau children are convex combinations of the parent's coefficients: every
+    child coefficient lies in [min b, max b] and the spread max - min never grows
+    (SPEC.md's subdivision-convergence property; the basis of the bounds)."""
+    rng = np.random.default_rng(12)
+    for _ in range(200):
+        b = rng.normal(size=27) * rng.uniform(0.1, 10.0)
+        lo, hi = b.min(), b.max()
+        eps = 4e-16 * np.max(np.abs(b))
+        for o in range(8):
+            c = oracle.subdivide(b, o)
+            assert c.min() >= lo - eps and c.max() <= hi + eps
+            assert c.max() - c.min() <= hi - lo + 2 * eps
+
+
 def test_subdivision_children_corners_are_values():
     """Child corner coefficients are actual values of the polynomial."""
     rng = np.random.default_rng(10)
