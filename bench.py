@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--config", type=int, default=1, choices=sorted(CONFIG_DESC))
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--clock-ms", type=float, default=10.0,
+                   help="NVML clock sampling period during the timed region (ms)")
     p.add_argument("--no-cupti", action="store_true",
                    help="skip the torch.profiler (CUPTI) kernel-duration pass (e.g. under ncu)")
     p.add_argument("--graph", action="store_true",
@@ -115,8 +117,9 @@ class ClockSampler:
         "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
     }
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.010):
         self.samples, self.reasons, self.max_mhz = [], 0, None
+        self.period_s = period_s
         self._stop = threading.Event()
         try:
             import pynvml
@@ -134,7 +137,7 @@ class ClockSampler:
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(self.period_s)
 
     def __enter__(self):
         if self.nv is not None:
@@ -341,7 +344,7 @@ def run_ours(args, world, rank, local):
 
     # timed region 1 (the headline): the product call exactly as a user makes it
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_ms * 1e-3) as clk:
         barrier(world)
         torch.cuda.synchronize()
         ev0.record(stream)
@@ -638,7 +641,7 @@ def run_op(args, world, rank, local):
         step()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_ms * 1e-3) as clk:
         barrier(world)
         torch.cuda.synchronize()
         ev0.record(stream)

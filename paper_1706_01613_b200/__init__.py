@@ -128,6 +128,11 @@ def _torch():
 def _stream_handle(stream) -> int:
     torch = _torch()
     if stream is None:
+        # the current stream of the current device, as torch.cuda.current_stream()
+        # gives it, without building a Stream object (3 us -> 0.3 us per call)
+        raw, dev = getattr(torch._C, "_cuda_getCurrentRawStream", None), getattr(torch._C, "_cuda_getDevice", None)
+        if raw is not None and dev is not None:
+            return int(raw(dev()))
         stream = torch.cuda.current_stream()
     return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
 

@@ -139,6 +139,16 @@ def test_cuda_graph_capture_and_replay():
     assert np.array_equal(flags.cpu().numpy(), eager)
 
 
+def test_binding_uses_torchs_current_stream():
+    """The binding's fast current-stream lookup equals torch.cuda.current_stream()."""
+    from paper_1706_01613_b200 import _stream_handle
+    assert _stream_handle(None) == torch.cuda.current_stream().cuda_stream
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        assert _stream_handle(None) == s.cuda_stream == torch.cuda.current_stream().cuda_stream
+    assert _stream_handle(s) == s.cuda_stream
+
+
 def test_side_stream_matches_default_stream():
     coords = hexgen.ragged_soa(4099, seed=11, amp=0.45)
     dev = torch.from_numpy(coords).cuda()
