@@ -485,7 +485,11 @@ __global__ void __launch_bounds__(WT_THREADS, 2)
 // current tile; cp.async.wait_group blocks in hardware (no spinning) and no
 // block barrier is needed because every thread reads only what it copied.
 // ---------------------------------------------------------------------------
-constexpr int CP_THREADS = 256;
+#ifndef HEXVAL_CP_THREADS
+#define HEXVAL_CP_THREADS 256
+#endif
+constexpr int CP_THREADS = HEXVAL_CP_THREADS;        // A/B builds: 128 x 4 or 256 x 2 CTAs/SM (16 warps/SM)
+constexpr int CP_MINB = 512 / CP_THREADS;
 constexpr size_t CP_SMEM = (size_t)2 * 24 * CP_THREADS * sizeof(double);   // 96 KB: two tiles
 
 __device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, uint64_t policy) {
@@ -533,7 +537,7 @@ struct Pass1Body {                                           // K1/K2: S1-S8 + K
 };
 
 template <class Body>
-__global__ void __launch_bounds__(CP_THREADS, 2)
+__global__ void __launch_bounds__(CP_THREADS, CP_MINB)
     soa_cp_kernel(const double* __restrict__ coords, int64_t n, Body body) {
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS]
     const int tid = threadIdx.x;
@@ -601,7 +605,7 @@ __device__ __forceinline__ void cp_gather_row(const double* __restrict__ verts, 
 }
 
 template <class Body>
-__global__ void __launch_bounds__(CP_THREADS, 2)
+__global__ void __launch_bounds__(CP_THREADS, CP_MINB)
     idx_cp_kernel(const double* __restrict__ verts, const int32_t* __restrict__ idx, int64_t n, Body body) {
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS] coords, then [2][CP_THREADS][8] ids
     const int tid = threadIdx.x;
