@@ -191,6 +191,18 @@ __device__ __forceinline__ int step2_class(const Samples& s, double tau2) {
     for (int e = 0; e < 12; ++e) km = min(km, key(s.d[e]));
     if (km > T) return ST_VALID;                       // every sample > tau2 > 0: robustly positive
     if (!INT_SLOW) {
+#ifndef HEXVAL_STEP2_NO_NEGKEY
+        // robustly negative sample first (one unsigned max over the keys: the sign bit
+        // makes negatives exceed positives, then larger magnitude = larger key):
+        // |x| > tau2 whenever its hi word exceeds tau2's, so the verdict is the one
+        // the compares below would reach; most INVALID hexes stop here
+        unsigned um = (unsigned)key(s.c[0]);
+#pragma unroll
+        for (int k = 1; k < 8; ++k) um = max(um, (unsigned)key(s.c[k]));
+#pragma unroll
+        for (int e = 0; e < 12; ++e) um = max(um, (unsigned)key(s.d[e]));
+        if (um > (0x80000000u | (unsigned)T)) return ST_INVALID;
+#endif
         bool neg = false, amb = false;
 #pragma unroll
         for (int k = 0; k < 8; ++k) { neg |= s.c[k] < -tau2; amb |= fabs(s.c[k]) <= tau2; }
