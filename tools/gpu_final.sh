@@ -10,6 +10,7 @@ timeout 900 python bench.py > $O/bench.log 2>&1
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.log 2>&1
 for c in 2 3 4; do timeout 900 python bench.py --config $c --steps $([ $c = 4 ] && echo 3 || echo 20) --no-e2e > $O/bench_c$c.log 2>&1; done
 timeout 900 python bench.py --config 0 --steps 500 --warmup 20 --graph --no-e2e > $O/bench_c0.log 2>&1
+timeout 900 python bench.py --config 1 --coeffs --steps 50 --no-e2e --no-cpu-baseline > $O/bench_c1_coeffs.log 2>&1
 timeout 600 python tools/timing_probe.py --config 1 > $O/probe_c1.json 2> $O/probe_c1.err
 for c in 1 3; do timeout 900 python bench.py --op quality --config $c --steps 50 > $O/quality_c$c.log 2>&1; done
 for c in 1 3; do timeout 900 python bench.py --op screen --config $c --steps 50 > $O/screen_c$c.log 2>&1; done
