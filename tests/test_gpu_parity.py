@@ -443,6 +443,22 @@ def test_config3_full_size_sampled():
     assert st["n_valid"] + st["n_invalid"] + st["n_undetermined"] + st["n_nonfinite"] == n
 
 
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_full_size_every_hex_against_the_oracle(cfg):
+    """Configs 1-3 at full size, every hex (not a sample): the oracle runs on all host
+    cores (about 6 M hex/s), so the whole config is compared bit for bit, and the
+    near-boundary count must be 0 (BASELINE.json north star)."""
+    if cfg == 1:
+        _, coords = hexgen.make(1)
+        f, _ = gpu_soa(coords)
+        ref = oracle.check_soa(coords)
+    else:
+        _, verts, idx = hexgen.make(cfg)
+        f, _ = gpu_indexed(verts, idx)
+        ref = oracle.check_indexed(verts, idx)
+    assert_flags_match(f, ref)
+
+
 def test_config4_full_size_closed_form_and_sampled():
     _, coords, r = hexgen.make(4)
     stats = hv.Stats()
