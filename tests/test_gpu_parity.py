@@ -450,8 +450,9 @@ def test_full_size_every_hex_against_the_oracle(cfg):
     near-boundary count must be 0 (BASELINE.json north star)."""
     if cfg == 1:
         _, coords = hexgen.make(1)
-        f, _ = gpu_soa(coords)
-        ref = oracle.check_soa(coords)
+        f, k = gpu_soa(coords, coeffs=True)
+        ref = oracle.check_soa(coords, want_coeffs=True)
+        assert_coeffs_match(k, ref["coeffs"], f)             # all 270M coefficients, 1e-12 x max|b|
     else:
         _, verts, idx = hexgen.make(cfg)
         f, _ = gpu_indexed(verts, idx)
