@@ -622,6 +622,57 @@ def _bounds_parity(coords, rel_tol, lo, up, st):
     return ref
 
 
+def _bounds_parity_vec(coords, rel_tol, lo, up, st):
+    """_bounds_parity without per-hex Python work (full-size inputs): tol from the oracle's
+    root coefficients."""
+    ref = oracle.min_detj_bounds_soa(coords, rel_tol)
+    nf = np.isnan(ref["lower"])
+    assert np.array_equal(np.isnan(lo), nf) and np.array_equal(np.isnan(up), nf)
+    ok = ~nf
+    b = oracle.check_soa(coords, want_coeffs=True)["coeffs"]
+    tol = rel_tol * np.abs(b).max(axis=0)
+    eps = 1e-12 * np.maximum(1.0, np.abs(np.where(ok, up, 0.0)))
+    tight = ok & ~(((st & 1) == 1) | (ref["capped"] == 1))
+    assert np.all(up[tight] - lo[tight] <= tol[tight] + eps[tight])
+    assert np.all(lo[ok] <= ref["upper"][ok] + eps[ok]) and np.all(ref["lower"][ok] <= up[ok] + eps[ok])
+    assert np.all(np.abs(up[tight] - ref["upper"][tight]) <= tol[tight] + eps[tight])
+    assert np.all(np.abs(lo[tight] - ref["lower"][tight]) <= tol[tight] + eps[tight])
+
+
+@pytest.mark.parametrize("row", ["quality", "bounds", "quads", "select"])
+def test_next_rows_full_size_every_item(row):
+    """Each NEXT row at its bench workload size, compared on every item (the oracle runs on
+    all host cores)."""
+    if row == "quads":
+        coords = hexgen.quad_soa(10_000_000, 0.35, 5)
+        f, J = hv.check_quad_soa(torch.from_numpy(coords).cuda(), J=True)
+        torch.cuda.synchronize()
+        ref = oracle.check_quad_soa(coords)
+        assert np.array_equal(f.cpu().numpy(), ref["flags"]) and np.array_equal(J.cpu().numpy(), ref["J"])
+        return
+    if row == "select":
+        _, verts, idx = hexgen.make(3)
+        f, _ = gpu_indexed(verts, idx)
+        n = idx.shape[0]
+        grp = (np.arange(n) % 99 ** 3).astype(np.int32)
+        ids, c, counts = hv.select_valid(torch.from_numpy(f).cuda(), torch.from_numpy(grp).cuda(), 99 ** 3)
+        torch.cuda.synchronize()
+        ref_ids, ref_counts = oracle.select_valid(f, grp, 99 ** 3)
+        assert c == ref_ids.size and np.array_equal(ids.cpu().numpy(), ref_ids)
+        assert np.array_equal(counts.cpu().numpy(), ref_counts)
+        return
+    _, coords = hexgen.make(1)
+    dev = torch.from_numpy(coords).cuda()
+    if row == "quality":
+        sj, t1 = hv.corner_quality_soa(dev)
+        torch.cuda.synchronize()
+        _quality_parity(coords, sj.cpu().numpy(), t1.cpu().numpy())
+    else:
+        lo, up, st = hv.min_detj_bounds_soa(dev, 1e-3)
+        torch.cuda.synchronize()
+        _bounds_parity_vec(coords, 1e-3, lo.cpu().numpy(), up.cpu().numpy(), st.cpu().numpy())
+
+
 @pytest.mark.parametrize("rel_tol", [1e-2, 1e-5])
 def test_min_detj_bounds_random(rel_tol):
     coords = hexgen.ragged_soa(5003, seed=41, amp=0.5)
