@@ -17,3 +17,17 @@ def pytest_configure(config):
 def golden_hexes():
     from tests.pins import load_golden
     return {name: load_golden(name) for name in ("fig5_invalid", "fig6_valid", "fig7_invalid")}
+
+
+@pytest.fixture(autouse=True)
+def _release_cuda_cache(request):
+    """Full-size GPU tests allocate tens of GB; hand cached blocks back between tests."""
+    yield
+    if request.node.get_closest_marker("gpu") is not None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                torch.cuda.synchronize()
+                torch.cuda.empty_cache()
+        except Exception:
+            pass
