@@ -8,6 +8,7 @@ configuration bench.py times; the oracle checks a sample of the outputs
 (random hexes plus every hex that took the exact-sign or subdivision path)
 and, for config 4, the closed-form verdict of every hex.
 """
+import functools
 import os
 
 import numpy as np
@@ -26,6 +27,13 @@ if not torch.cuda.is_available():
 import paper_1706_01613_b200 as hv  # noqa: E402
 
 COEFF_TOL = 1e-12
+
+
+@functools.lru_cache(maxsize=None)
+def full_config(cfg: int):
+    """hexgen.make(cfg), generated once per session (configs 1-3 take seconds to tens of
+    seconds on the host); callers must not modify the arrays."""
+    return hexgen.make(cfg)
 
 
 def gpu_soa(coords: np.ndarray, coeffs=False, stats=None):
@@ -408,7 +416,7 @@ def _sample(n, flags, k, seed):
 
 
 def test_config1_full_size_sampled():
-    _, coords = hexgen.make(1)
+    _, coords = full_config(1)
     n = coords.shape[1]
     stats = hv.Stats()
     f, _ = gpu_soa(coords, stats=stats)
@@ -422,7 +430,7 @@ def test_config1_full_size_sampled():
 
 
 def test_config2_full_size_sampled():
-    _, verts, idx = hexgen.make(2)
+    _, verts, idx = full_config(2)
     f, _ = gpu_indexed(verts, idx)
     sel = _sample(idx.shape[0], f, 30000, 2)
     ref = oracle.check_indexed(verts, idx[sel])
@@ -430,7 +438,7 @@ def test_config2_full_size_sampled():
 
 
 def test_config3_full_size_sampled():
-    _, verts, idx = hexgen.make(3)
+    _, verts, idx = full_config(3)
     stats = hv.Stats()
     f, _ = gpu_indexed(verts, idx, stats=stats)
     n = idx.shape[0]
@@ -449,12 +457,12 @@ def test_full_size_every_hex_against_the_oracle(cfg):
     cores (about 6 M hex/s), so the whole config is compared bit for bit, and the
     near-boundary count must be 0 (BASELINE.json north star)."""
     if cfg == 1:
-        _, coords = hexgen.make(1)
+        _, coords = full_config(1)
         f, k = gpu_soa(coords, coeffs=True)
         ref = oracle.check_soa(coords, want_coeffs=True)
         assert_coeffs_match(k, ref["coeffs"], f)             # all 270M coefficients, 1e-12 x max|b|
     else:
-        _, verts, idx = hexgen.make(cfg)
+        _, verts, idx = full_config(cfg)
         f, _ = gpu_indexed(verts, idx)
         ref = oracle.check_indexed(verts, idx)
     assert_flags_match(f, ref)
@@ -564,10 +572,10 @@ def test_test1_is_necessary_at_full_size(cfg):
     config, no hex the robust check calls VALID fails Test 1 (a property that holds at
     any size, checked on every hex through the fused screening call)."""
     if cfg == 1:
-        _, coords = hexgen.make(1)
+        _, coords = full_config(1)
         f, sj, t1 = hv.check_screen_soa(torch.from_numpy(coords).cuda())
     else:
-        verts, idx = hexgen.indexed_config(3)
+        _, verts, idx = full_config(3)
         f, sj, t1 = hv.check_screen_indexed(torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda())
     torch.cuda.synchronize()
     valid = (f & 3) == hv.VALID
@@ -651,7 +659,7 @@ def test_next_rows_full_size_every_item(row):
         assert np.array_equal(f.cpu().numpy(), ref["flags"]) and np.array_equal(J.cpu().numpy(), ref["J"])
         return
     if row == "select":
-        _, verts, idx = hexgen.make(3)
+        _, verts, idx = full_config(3)
         f, _ = gpu_indexed(verts, idx)
         n = idx.shape[0]
         grp = (np.arange(n) % 99 ** 3).astype(np.int32)
@@ -661,7 +669,7 @@ def test_next_rows_full_size_every_item(row):
         assert c == ref_ids.size and np.array_equal(ids.cpu().numpy(), ref_ids)
         assert np.array_equal(counts.cpu().numpy(), ref_counts)
         return
-    _, coords = hexgen.make(1)
+    _, coords = full_config(1)
     dev = torch.from_numpy(coords).cuda()
     if row == "quality":
         sj, t1 = hv.corner_quality_soa(dev)
