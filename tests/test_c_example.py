@@ -44,3 +44,21 @@ def test_example_runs_on_gpu(tmp_path):
     host = [l.split(": ")[1].split()[0] for l in out.stdout.splitlines() if l.startswith("host")]
     dev = [l.split(": ")[1].split()[0] for l in out.stdout.splitlines() if l.startswith("device")]
     assert host == want and dev == want, out.stdout
+
+
+@pytest.mark.gpu
+def test_python_mesh_example_runs_on_gpu(tmp_path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "examples"))
+    import numpy as np
+    import check_mesh
+    verts, idx = check_mesh.jittered_grid(20, 0.45, 1)
+    np.savez(tmp_path / "m.npz", vertices=verts, hex_idx=idx)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "examples", "check_mesh.py"), str(tmp_path / "m.npz")],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "8000 hexahedra" in out.stdout and "must be 0" in out.stdout
+    assert "(on valid ones: 0, must be 0)" in out.stdout
