@@ -57,7 +57,7 @@ def main(argv):
     print(f"  Test 1 fails on {int((t1 == 0).sum().item())} (on valid ones: {t1_fail_valid}, must be 0)")
     ok = (flags & 3) == hv.VALID
     if ok.any():
-        print(f"  min corner scaled Jacobian over valid hexes: {float(sj[ok].min()):.4f}")
+        print(f"  min corner scaled Jacobian over valid hexes: {float(sj[ok].min()):.4g}")
     bad = torch.nonzero((flags & 3) != hv.VALID).flatten()
     if bad.numel():
         sub = x[bad.to(torch.int64)].contiguous()
