@@ -86,7 +86,11 @@ struct Ctl {                 // per-call control block (device scratch)
 // loaders: SoA planes or indexed gather
 // ---------------------------------------------------------------------------
 struct SoaLoader {
+#ifdef HEXVAL_SOA_INT_STEP2
+    static constexpr bool kIntStep2 = true;      // A/B build: integer-pipe slow path for SoA too
+#else
     static constexpr bool kIntStep2 = false;     // see step2_class
+#endif
     const double* __restrict__ coords;
     int64_t n;
     // pass 1: streamed once, evict-first
