@@ -145,6 +145,11 @@ def _require(t, dtype, name: str, ndim: int | None = None):
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (use check_*_host for host memory)")
+    cur = getattr(torch._C, "_cuda_getDevice", None)
+    if t.device.index != (cur() if cur is not None else torch.cuda.current_device()):
+        # the library launches on the current device and stream: make them the tensor's
+        raise ValueError(f"{name} is on {t.device}, the current device is cuda:{torch.cuda.current_device()} "
+                         f"(call under torch.cuda.device({t.device}))")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     if ndim is not None and t.dim() != ndim:
