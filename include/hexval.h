@@ -93,6 +93,8 @@ typedef struct hexval_profile hexval_profile;
  *              after the stream synchronises.  No host synchronisation
  *              happens inside the call.  Calls on different streams are
  *              independent (scratch is stream-ordered cudaMallocAsync).
+ * Device       the calling thread's current device (cudaSetDevice): every
+ *              device buffer and the stream must belong to it.
  * Ownership    the caller owns every buffer; the library never frees them.
  * n == 0       returns HEXVAL_OK without enqueueing work.
  * Returns      HEXVAL_OK or a negative status (see above).  Data problems
