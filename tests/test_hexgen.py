@@ -67,3 +67,16 @@ def test_adversarial_closed_form_minimum():
             m = pins.detj(x, G[:, perm]).min() / vol
             best = m if best is None else min(best, m)
         assert abs(best - rr) < 2e-6
+
+
+def test_verdict_mix_matches_the_survey_recipe():
+    """The synthetic configs reproduce SURVEY.md 8(d)'s first-pass mix (App. B.1), checked
+    with the oracle on prefix samples: config 1 ~4.9% INVALID, config 3 ~35.6% INVALID."""
+    import oracle
+    c1 = hexgen.soa_config(40_000, 0.35, 1)
+    f1 = oracle.check_soa(c1)["flags"] & 3
+    assert 0.040 < np.mean(f1 == oracle.INVALID) < 0.060
+    assert np.mean(f1 == oracle.VALID) > 0.94
+    verts, idx = hexgen.indexed_config(3, start=0, count=40_000)
+    f3 = oracle.check_indexed(verts, idx)["flags"] & 3
+    assert 0.32 < np.mean(f3 == oracle.INVALID) < 0.40
