@@ -117,6 +117,10 @@ def lib():
         L.oracle_check_quad_soa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                             ctypes.c_void_p, ctypes.c_int]
         L.oracle_check_quad_soa.restype = None
+        L.oracle_sample_tau.argtypes = [_D, ctypes.c_int]
+        L.oracle_sample_tau.restype = ctypes.c_double
+        L.oracle_tau_depth.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_int]
+        L.oracle_tau_depth.restype = ctypes.c_double
         L.oracle_num_threads.argtypes = [ctypes.c_int]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
@@ -196,6 +200,17 @@ def classify_coeffs(b, E: float = 1.0) -> dict:
     r = OracleResult()
     lib().oracle_classify_coeffs(_dptr(b), float(E), ctypes.byref(r))
     return r.as_dict()
+
+
+def sample_tau(X, sigma: int) -> float:
+    """Bound on the rounding error of samples27(X)[sigma] (the Step-2 exact-fallback threshold)."""
+    X = _hex(X)
+    return lib().oracle_sample_tau(_dptr(X), int(sigma))
+
+
+def tau_depth(E: float, Mb: float, depth: int) -> float:
+    """Near-boundary bound on a Bezier value at subdivision depth `depth` (reading G14)."""
+    return lib().oracle_tau_depth(float(E), float(Mb), int(depth))
 
 
 def num_threads(nthreads: int = 0) -> int:

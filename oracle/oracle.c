@@ -428,10 +428,16 @@ typedef struct {
 } rec_ctx;
 
 /* Combined (oracle + any implementation of the same bound) rounding-error
- * bound for a Bezier value at subdivision depth d. */
+ * bound for a Bezier value at subdivision depth d:
+ * E = max |edge-vector component| of the hex, Mb = max |b_root|.  Pinned
+ * against exact rational arithmetic by tests/test_tau_bounds.py. */
+double oracle_tau_depth(double E, double Mb, int depth) {
+    return 16384.0 * U_ROUND * E * E * E + 16.0 * depth * U_ROUND * Mb +
+           ldexp(1.0, -1040) * (1.0 + E * E);
+}
+
 static double tau_depth(const rec_ctx* ctx, int depth) {
-    return 16384.0 * U_ROUND * ctx->E * ctx->E * ctx->E + 16.0 * depth * U_ROUND * ctx->Mb +
-           ldexp(1.0, -1040) * (1.0 + ctx->E * ctx->E);
+    return oracle_tau_depth(ctx->E, ctx->Mb, depth);
 }
 
 static void note_decision(rec_ctx* ctx, double value, int depth) {
@@ -490,6 +496,24 @@ static int coord_ok(double x) {
     return isfinite(x) && fabs(x) <= 0x1p300;
 }
 
+/* Rounding-error bound of the oracle's fp det J sample from the componentwise
+ * magnitudes Ja of its Jacobian columns (triple product with
+ * rounded inputs, 32 u perm(|J|), plus an underflow term).  Decides when Step 2
+ * falls back to the exact sign (reading G8); pinned by tests/test_tau_bounds.py. */
+static double sample_tau(const double Ja[3][3]) {
+    const double dmax = max_abs3x3(Ja);
+    return 32.0 * U_ROUND * permanent_abs(Ja) + ldexp(1.0, -1060) * (1.0 + 6.0 * dmax * dmax);
+}
+
+double oracle_sample_tau(const double X[8][3], int sigma) {
+    edges_t Ev;
+    double xi[3], J[3][3], Ja[3][3];
+    edge_vectors(X, &Ev);
+    oracle_node_xi(sigma, xi);
+    derivatives(&Ev, xi, J, Ja);
+    return sample_tau(Ja);
+}
+
 int oracle_check_hex(const double X[8][3], oracle_result* r) {
     memset(r, 0, sizeof(*r));
     r->margin_ratio = INFINITY;
@@ -523,8 +547,7 @@ int oracle_check_hex(const double X[8][3], oracle_result* r) {
         oracle_node_xi(s, xi);
         derivatives(&Ev, xi, J, Ja);
         r->c[s] = det_eps(J);
-        const double dmax = max_abs3x3(Ja);
-        tau_c[s] = 32.0 * U_ROUND * permanent_abs(Ja) + ldexp(1.0, -1060) * (1.0 + 6.0 * dmax * dmax);
+        tau_c[s] = sample_tau(Ja);
     }
 
     /* Step 2: if at least one of the 20 values is <= 0, return False.  Values

@@ -68,6 +68,14 @@ void   oracle_subdivide(const double b[27], int child, double out[27]);/* de Cas
 int    oracle_exact_sign(const double X[8][3], int sigma);             /* sign of det J(xi_sigma), exact */
 void   oracle_node_xi(int sigma, double xi[3]);                        /* xi_sigma */
 int    oracle_num_threads(int nthreads);
+/* Rounding-error bounds used by the readings G8 / G14:
+ *   oracle_sample_tau   bound on |fl(det J(xi_sigma)) - det J(xi_sigma)| of oracle_samples27's
+ *                       value; Step 2 re-decides a sample exactly when |c| <= it;
+ *   oracle_tau_depth    combined bound (this oracle and the CUDA path) on a Bezier value at
+ *                       subdivision depth `depth` of a hex with edge scale E and max |b_root| Mb;
+ *                       a decision with |value| <= it marks the hex near-boundary. */
+double oracle_sample_tau(const double X[8][3], int sigma);
+double oracle_tau_depth(double E, double Mb, int depth);
 /* Steps 4-5 on a given coefficient vector; E sets tau. */
 int    oracle_classify_coeffs(const double b[27], double E, oracle_result* r);
 
