@@ -134,7 +134,10 @@ int hexval_classify_bezier(const double* coeffs, int64_t n, uint8_t* flags_out,
  *                      corner edge has zero length or the hex is NONFINITE;
  *   test1_out_opt[i]   1 iff det J > 0 at all 8 corners (Ushakova's Test 1, the 8 corner
  *                      tetrahedra: a necessary condition only, PAPER.md:107-109,
- *                      1260-1263), fp64 sign of the corner sample.
+ *                      1260-1263), each sign exact: a corner sample within its fp64
+ *                      rounding bound of 0 is re-decided in exact arithmetic (the
+ *                      coincident-node rule, then the long accumulator of Step 2), so
+ *                      a corner det J that is exactly 0 fails the test.
  * Asynchronous on `stream`; returns HEXVAL_OK or a negative status.              */
 int hexval_corner_quality_soa(const double* coords, int64_t n, double* sj_min_out_opt,
                               uint8_t* test1_out_opt, cudaStream_t stream);

@@ -105,6 +105,9 @@ def lib():
         L.oracle_corner_quality_soa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                                 ctypes.c_void_p, ctypes.c_int]
         L.oracle_corner_quality_soa.restype = None
+        L.oracle_corner_quality_indexed.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        L.oracle_corner_quality_indexed.restype = None
         L.oracle_min_detj_bounds.argtypes = [_D, ctypes.c_double, ctypes.POINTER(OracleBounds)]
         L.oracle_min_detj_bounds.restype = None
         L.oracle_min_detj_bounds_soa.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p,
@@ -270,6 +273,18 @@ def corner_quality_soa(coords: np.ndarray, nthreads: int = 0) -> dict:
     nr = np.zeros(n, np.uint8)
     lib().oracle_corner_quality_soa(coords.ctypes.data, n, sj.ctypes.data, t1.ctypes.data, nr.ctypes.data,
                                     int(nthreads))
+    return {"sj_min": sj, "test1": t1, "near": nr}
+
+
+def corner_quality_indexed(vertices: np.ndarray, hex_idx: np.ndarray, nthreads: int = 0) -> dict:
+    vertices = np.ascontiguousarray(vertices, dtype=np.float64)
+    hex_idx = np.ascontiguousarray(hex_idx, dtype=np.int32)
+    n = hex_idx.shape[0]
+    sj = np.zeros(n)
+    t1 = np.zeros(n, np.uint8)
+    nr = np.zeros(n, np.uint8)
+    lib().oracle_corner_quality_indexed(vertices.ctypes.data, hex_idx.ctypes.data, n, sj.ctypes.data,
+                                        t1.ctypes.data, nr.ctypes.data, int(nthreads))
     return {"sj_min": sj, "test1": t1, "near": nr}
 
 

@@ -720,9 +720,16 @@ void oracle_corner_quality(const double X[8][3], double* sj_min, int* test1, int
         oracle_node_xi(k, xi);
         derivatives(&E, xi, J, Ja);
         const double d = det_eps(J);
-        const double tau = 32.0 * U_ROUND * permanent_abs(Ja) + ldexp(1.0, -1060);
-        if (fabs(d) <= tau) nr = 1;
-        if (oracle_exact_sign(X, k) <= 0) all_pos = 0;
+        /* reading G8, as in Step 2: a corner value within its rounding bound of 0
+         * (sample_tau, pinned by tests/test_tau_bounds.py) takes its exact sign;
+         * outside it the fp sign is the exact sign */
+        const double tau = sample_tau(Ja);
+        if (fabs(d) <= tau) {
+            nr = 1;
+            if (oracle_exact_sign(X, k) <= 0) all_pos = 0;
+        } else if (d < 0.0) {
+            all_pos = 0;
+        }
         double len[3];
         for (int r = 0; r < 3; ++r) len[r] = sqrt(J[r][0] * J[r][0] + J[r][1] * J[r][1] + J[r][2] * J[r][2]);
         if (len[0] == 0.0 || len[1] == 0.0 || len[2] == 0.0) undefined = 1;
@@ -743,6 +750,24 @@ void oracle_corner_quality_soa(const double* coords, int64_t n, double* sj_out, 
         double X[8][3];
         for (int k = 0; k < 8; ++k)
             for (int a = 0; a < 3; ++a) X[k][a] = coords[(int64_t)(3 * k + a) * n + i];
+        double sj;
+        int t1, nr;
+        oracle_corner_quality(X, &sj, &t1, &nr);
+        if (sj_out) sj_out[i] = sj;
+        if (test1_out) test1_out[i] = (uint8_t)t1;
+        if (near_out) near_out[i] = (uint8_t)nr;
+    }
+}
+
+void oracle_corner_quality_indexed(const double* vertices, const int32_t* hex_idx, int64_t n, double* sj_out,
+                                   uint8_t* test1_out, uint8_t* near_out, int nthreads) {
+    const int nt = oracle_num_threads(nthreads);
+    (void)nt;
+#pragma omp parallel for schedule(dynamic, 256) num_threads(nt)
+    for (int64_t i = 0; i < n; ++i) {
+        double X[8][3];
+        for (int k = 0; k < 8; ++k)
+            for (int a = 0; a < 3; ++a) X[k][a] = vertices[(int64_t)hex_idx[i * 8 + k] * 3 + a];
         double sj;
         int t1, nr;
         oracle_corner_quality(X, &sj, &t1, &nr);

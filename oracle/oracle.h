@@ -106,6 +106,8 @@ void   oracle_min_detj_bounds_soa(const double* coords, int64_t n, double rel_to
                                   double* upper_out, uint8_t* capped_out, int nthreads);
 void   oracle_corner_quality_soa(const double* coords, int64_t n, double* sj_out, uint8_t* test1_out,
                                  uint8_t* near_out, int nthreads);
+void   oracle_corner_quality_indexed(const double* vertices, const int32_t* hex_idx, int64_t n, double* sj_out,
+                                     uint8_t* test1_out, uint8_t* near_out, int nthreads);
 
 /* NEXT-4, linear quadrangle: Q[k][a], nodes 1..4 counter-clockwise
  * (L1 = (1-xi)(1-eta), L2 = xi(1-eta), L3 = xi eta, L4 = (1-xi) eta).  J[k] = det J at

@@ -176,6 +176,31 @@ __device__ __forceinline__ bool IdxLoader::dup_face_pair(int64_t i) const {
     return hit;
 }
 
+// Test 1 in exact arithmetic for a hex whose corner samples are not all
+// robustly signed (corner_quality gave T1_PENDING): two nodes sharing a face
+// coincide => a corner sample is exactly 0 (face_pair_coincident) => fails;
+// else every corner within tau2 of 0 takes its exact sign (K5 long
+// accumulator).  Out of line; re-reads the hex's coordinates.
+template <class L>
+__device__ __noinline__ uint8_t exact_test1(const L ld, int64_t i) {
+    if (ld.dup_face_pair(i)) return 0;
+    double X[24];
+    ld.load(i, X);
+    if (face_pair_coincident(X)) return 0;
+    Samples s;
+    samples20(X, s);
+    const int T = key(step2_tau(s.ekey));
+#pragma unroll 1
+    for (int k = 0; k < 8; ++k) {
+        if (abskey(s.c[k]) <= T) {
+            if (exact_sample_sign(X, k) <= 0) return 0;
+        } else if (s.c[k] < 0.0) {
+            return 0;
+        }
+    }
+    return 1;
+}
+
 // Step 2 classification shared by pass 1 and the exact kernel.
 enum : int { ST_INVALID = 0, ST_VALID = 1, ST_NONFINITE = 3, ST_SUB = 4, ST_EXACT = 5 };
 
@@ -291,12 +316,18 @@ __device__ __forceinline__ double len2(const V3& v) {
     return __fma_rn(v.z, v.z, __fma_rn(v.y, v.y, __dmul_rn(v.x, v.x)));
 }
 
-// NEXT-2 per hex from the 12 edge vectors E (samples20 order) and the 8 corner
-// samples c: Test 1 (all c > 0) and the minimum corner scaled Jacobian
+// NEXT-2 per hex from the 12 edge vectors E (samples20 order), the 8 corner
+// samples c and the edge-scale key: Test 1 (all 8 corner det J > 0, PAPER.md:
+// 107-109, 1260-1263) and the minimum corner scaled Jacobian
 // c / (|d_xi x||d_eta x||d_zeta x|), the argmin taken by
 // cross-multiplication so only the winner pays a division and a sqrt.  Shared
 // by quality_kernel and the fused pass 1 (bit-identical outputs).
-__device__ __forceinline__ void corner_quality(const V3* E, const double* c, double& sj, uint8_t& t1) {
+// t1 = 1: every corner sample robustly positive; 0: some corner robustly
+// negative; T1_PENDING: some |c| <= tau2 (Step 2's rounding bound) and none
+// robustly negative -- the caller decides it in exact arithmetic (exact_test1).
+constexpr uint8_t T1_PENDING = 2;
+
+__device__ __forceinline__ void corner_quality(const V3* E, const double* c, int ekey, double& sj, uint8_t& t1) {
     const double l12 = len2(E[0]), l43 = len2(E[1]), l56 = len2(E[2]), l87 = len2(E[3]);
     const double l14 = len2(E[4]), l23 = len2(E[5]), l58 = len2(E[6]), l67 = len2(E[7]);
     const double l15 = len2(E[8]), l26 = len2(E[9]), l48 = len2(E[10]), l37 = len2(E[11]);
@@ -314,7 +345,15 @@ __device__ __forceinline__ void corner_quality(const V3* E, const double* c, dou
         const double nk = __dmul_rn(c[k], fabs(c[k]));
         if (__dmul_rn(nk, bp) < __dmul_rn(bn, P[k])) { bn = nk; bp = P[k]; }   // nk/P[k] < bn/bp
     }
-    t1 = km > 0;
+    const int T = key(step2_tau(ekey));                // tau2 > 0: key == abskey
+    if (km > T) {
+        t1 = 1;
+    } else {
+        unsigned um = (unsigned)key(c[0]);
+#pragma unroll
+        for (int k = 1; k < 8; ++k) um = max(um, (unsigned)key(c[k]));
+        t1 = um > (0x80000000u | (unsigned)T) ? 0 : T1_PENDING;   // a robustly negative corner, else exact
+    }
     sj = zero_edge ? __longlong_as_double(0x7ff8000000000000ll) : copysign(sqrt(__ddiv_rn(fabs(bn), bp)), bn);
 }
 
@@ -332,7 +371,7 @@ __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i
         st = ST_NONFINITE;
     } else {
         Samples s;
-        if (QUAL) samples20(X, s, [&](const V3* E, const double* c) { corner_quality(E, c, sj, t1); });
+        if (QUAL) samples20(X, s, [&](const V3* E, const double* c, int ek) { corner_quality(E, c, ek, sj, t1); });
         else samples20(X, s);                             // S1 + S2
         st = step2_class<L::kIntStep2>(s, step2_tau(s.ekey));   // S3 (Step 2)
         if (st == ST_EXACT && ld.dup_face_pair(i)) st = ST_INVALID;   // a sample is exactly 0
@@ -340,6 +379,7 @@ __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i
         transform(s, t);                                  // S4 (Step 3)
         if (st == ST_VALID && !step4_positive(t)) st = ST_SUB;   // S5 (Step 4)
         if (COEFFS) write_coeffs(coeffs, n, i, s, t);
+        if (QUAL && t1 == T1_PENDING) t1 = exact_test1(ld, i);
     }
     uint8_t f;
     switch (st) {
@@ -677,7 +717,7 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
 // ---------------------------------------------------------------------------
 
 template <class L>
-__global__ void __launch_bounds__(256) quality_kernel(L ld, int64_t n, double* __restrict__ sj_out,
+__global__ void __launch_bounds__(256, 2) quality_kernel(L ld, int64_t n, double* __restrict__ sj_out,
                                                        uint8_t* __restrict__ t1_out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -695,7 +735,11 @@ __global__ void __launch_bounds__(256) quality_kernel(L ld, int64_t n, double* _
         const double c[8] = {det3(v12, v14, v15), det3(v12, v23, v26), det3(v43, v23, v37), det3(v43, v14, v48),
                              det3(v56, v58, v15), det3(v56, v67, v26), det3(v87, v67, v37), det3(v87, v58, v48)};
         const V3 E[12] = {v12, v43, v56, v87, v14, v23, v58, v67, v15, v26, v48, v37};
-        corner_quality(E, c, sj, t1);
+        int ek = 0;
+#pragma unroll
+        for (int q = 0; q < 12; ++q) ek = max(ek, max(abskey(E[q].x), max(abskey(E[q].y), abskey(E[q].z))));
+        corner_quality(E, c, ek, sj, t1);
+        if (t1 == T1_PENDING) t1 = exact_test1(ld, i);
     }
     if (sj_out) __stcs(sj_out + i, sj);
     if (t1_out) __stcs(t1_out + i, t1);

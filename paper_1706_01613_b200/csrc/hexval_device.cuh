@@ -60,12 +60,13 @@ struct Samples {
 };
 
 struct NoCornerHook {
-    __device__ __forceinline__ void operator()(const V3*, const double*) const {}
+    __device__ __forceinline__ void operator()(const V3*, const double*, int) const {}
 };
 
-// corner(E, c): optional consumer of the 12 edge vectors E = {v12, v43, v56,
-// v87, v14, v23, v58, v67, v15, v26, v48, v37} and the 8 corner samples c,
-// called once they exist (the fused NEXT-2 screening outputs).
+// corner(E, c, ekey): optional consumer of the 12 edge vectors E = {v12, v43,
+// v56, v87, v14, v23, v58, v67, v15, v26, v48, v37}, the 8 corner samples c
+// and the edge-scale key, called once they exist (the fused NEXT-2 screening
+// outputs).
 template <class CornerHook = NoCornerHook>
 __device__ __forceinline__ void samples20(const double* X, Samples& s, CornerHook&& corner = CornerHook()) {
     const V3 n1{X[0], X[1], X[2]}, n2{X[3], X[4], X[5]}, n3{X[6], X[7], X[8]}, n4{X[9], X[10], X[11]};
@@ -93,7 +94,7 @@ __device__ __forceinline__ void samples20(const double* X, Samples& s, CornerHoo
     s.c[7] = det3(v87, v58, v48);
     {
         const V3 E[12] = {v12, v43, v56, v87, v14, v23, v58, v67, v15, v26, v48, v37};
-        corner(E, s.c);
+        corner(E, s.c, e);
     }
     // twice the mid-edge derivatives (each shared by two edges)
     const V3 Se0 = vadd(v14, v23), Se1 = vadd(v58, v67);   // d_eta  at xi=1/2, zeta=0/1

@@ -72,6 +72,25 @@ def assert_coeffs_match(gpu_coeffs, ref_coeffs, flags):
 # paper examples and closed forms through the C ABI
 # --------------------------------------------------------------------------
 
+def test_root_emulation_is_bit_exact():
+    """tests/gpu_emulation.py (the CPU emulation the tau pins of tests/test_tau_bounds.py use
+    for the CUDA path's values) reproduces the kernels' 27 root coefficients bit for bit:
+    random, high-noise, degenerate, 2^+-200-scaled and config-4 hexes."""
+    from tests import gpu_emulation as gemu
+    from tests.test_tau_bounds import _degenerate_hexes
+    X = np.concatenate([
+        hexgen.soa_to_nodes(hexgen.soa_config(600, 0.35, 61)),
+        hexgen.soa_to_nodes(hexgen.soa_config(300, 0.6, 62)),
+        np.stack(_degenerate_hexes(300, 63)),
+        hexgen.soa_to_nodes(hexgen.soa_config(200, 0.4, 64)) * 2.0 ** 200,
+        hexgen.soa_to_nodes(hexgen.soa_config(200, 0.4, 65)) * 2.0 ** -200,
+        hexgen.soa_to_nodes(hexgen.adversarial_config(400, 4, start=77_000)[0])])
+    coords = hexgen.nodes_to_soa(X)
+    _, k = gpu_soa(coords, coeffs=True)
+    emu = np.array([gemu.root_coeffs(X[i]) for i in range(X.shape[0])]).T
+    assert np.array_equal(k.view(np.uint64), emu.view(np.uint64))
+
+
 def test_paper_figures(golden_hexes):
     X = np.stack([golden_hexes[k][0] for k in ("fig5_invalid", "fig6_valid", "fig7_invalid")])
     coords = hexgen.nodes_to_soa(X)
@@ -512,8 +531,9 @@ def _quality_parity(coords, sj, t1):
     assert np.array_equal(np.isnan(sj), nan_ref)
     ok = ~nan_ref
     assert np.max(np.abs(sj[ok] - ref["sj_min"][ok]), initial=0.0) <= 1e-13
-    sure = ref["near"] == 0
-    assert np.array_equal(t1[sure], ref["test1"][sure])
+    # Test 1 is decided exactly on both sides (corner samples within the rounding bound take
+    # their exact sign): equal on every item, near-zero corners included
+    assert np.array_equal(t1, ref["test1"])
     return ref
 
 
@@ -679,6 +699,31 @@ def test_next_rows_full_size_every_item(row):
         lo, up, st = hv.min_detj_bounds_soa(dev, 1e-3)
         torch.cuda.synchronize()
         _bounds_parity_vec(coords, 1e-3, lo.cpu().numpy(), up.cpu().numpy(), st.cpu().numpy())
+
+
+@pytest.mark.parametrize("op", ["quality", "screen"])
+def test_test1_exact_on_every_config3_candidate(op):
+    """NEXT-2 on all 40M config-3 candidates (18% have a duplicate vertex, many a corner
+    det J exactly 0): Test 1 equals the oracle's exact-sign Test 1 on every item, for the
+    standalone screening kernel and the fused validity + screening pass; the scaled
+    Jacobian matches where it is defined."""
+    _, verts, idx = full_config(3)
+    v, i = torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda()
+    if op == "quality":
+        sj, t1 = hv.corner_quality_indexed(v, i)
+    else:
+        _, sj, t1 = hv.check_screen_indexed(v, i)
+    torch.cuda.synchronize()
+    sj, t1 = sj.cpu().numpy(), t1.cpu().numpy()
+    n = idx.shape[0]
+    step = 8_000_000
+    for a in range(0, n, step):
+        ref = oracle.corner_quality_indexed(verts, idx[a:a + step])
+        assert np.array_equal(t1[a:a + step], ref["test1"]), a
+        nan_ref = np.isnan(ref["sj_min"])
+        s = sj[a:a + step]
+        assert np.array_equal(np.isnan(s), nan_ref)
+        assert np.max(np.abs(s[~nan_ref] - ref["sj_min"][~nan_ref]), initial=0.0) <= 1e-13
 
 
 @pytest.mark.parametrize("rel_tol", [1e-2, 1e-5])
