@@ -137,7 +137,7 @@ def _stream_handle(stream) -> int:
     return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def _require(t, dtype, name: str, ndim: int | None = None):
+def _require(t, dtype, name: str, ndim: int | None = None, shape: tuple | None = None):
     torch = _torch()
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
@@ -154,6 +154,27 @@ def _require(t, dtype, name: str, ndim: int | None = None):
         raise ValueError(f"{name} must be contiguous")
     if ndim is not None and t.dim() != ndim:
         raise ValueError(f"{name} must have {ndim} dims")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        # the kernels write exactly this many elements: a smaller buffer would be overrun
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+def _soa_input(coords, planes: int = 24) -> int:
+    torch = _torch()
+    _require(coords, torch.float64, "coords", 2)
+    if coords.shape[0] != planes:
+        raise ValueError(f"coords must have shape ({planes}, n)")
+    return coords.shape[1]
+
+
+def _indexed_inputs(vertices, hex_idx) -> int:
+    """(nv, 3) float64 vertices and (n, 8) int32 connectivity on the current device; returns n."""
+    torch = _torch()
+    _require(vertices, torch.float64, "vertices", 2)
+    _require(hex_idx, torch.int32, "hex_idx", 2)
+    if vertices.shape[1] != 3 or hex_idx.shape[1] != 8:
+        raise ValueError("vertices must be (nv, 3) and hex_idx (n, 8)")
+    return hex_idx.shape[0]
 
 
 class Stats:
@@ -214,19 +235,16 @@ def check_soa(coords, flags=None, coeffs=None, stats: Stats | None = None,
     (default: torch's current stream).
     """
     torch = _torch()
-    _require(coords, torch.float64, "coords", 2)
-    if coords.shape[0] != 24:
-        raise ValueError("coords must have shape (24, n)")
-    n = coords.shape[1]
+    n = _soa_input(coords)
     if flags is None:
         flags = torch.empty(n, dtype=torch.uint8, device=coords.device)
-    _require(flags, torch.uint8, "flags")
+    _require(flags, torch.uint8, "flags", shape=(n,))
     if coeffs is True:
         coeffs = torch.empty((27, n), dtype=torch.float64, device=coords.device)
     elif coeffs is False:
         coeffs = None
     if coeffs is not None:
-        _require(coeffs, torch.float64, "coeffs")
+        _require(coeffs, torch.float64, "coeffs", shape=(27, n))
     rc = lib().hexval_check_soa_ex(coords.data_ptr(), n, flags.data_ptr(),
                                    coeffs.data_ptr() if coeffs is not None else None,
                                    stats.ptr() if stats is not None else None,
@@ -240,20 +258,16 @@ def check_indexed(vertices, hex_idx, flags=None, coeffs=None, stats: Stats | Non
                   profile: Profile | None = None, stream=None):
     """hexval_check_indexed(_ex): vertices (nv, 3) float64, hex_idx (n, 8) int32, CUDA tensors."""
     torch = _torch()
-    _require(vertices, torch.float64, "vertices", 2)
-    _require(hex_idx, torch.int32, "hex_idx", 2)
-    if vertices.shape[1] != 3 or hex_idx.shape[1] != 8:
-        raise ValueError("vertices must be (nv, 3) and hex_idx (n, 8)")
-    n = hex_idx.shape[0]
+    n = _indexed_inputs(vertices, hex_idx)
     if flags is None:
         flags = torch.empty(n, dtype=torch.uint8, device=hex_idx.device)
-    _require(flags, torch.uint8, "flags")
+    _require(flags, torch.uint8, "flags", shape=(n,))
     if coeffs is True:
         coeffs = torch.empty((27, n), dtype=torch.float64, device=hex_idx.device)
     elif coeffs is False:
         coeffs = None
     if coeffs is not None:
-        _require(coeffs, torch.float64, "coeffs")
+        _require(coeffs, torch.float64, "coeffs", shape=(27, n))
     rc = lib().hexval_check_indexed_ex(vertices.data_ptr(), hex_idx.data_ptr(), n, flags.data_ptr(),
                                        coeffs.data_ptr() if coeffs is not None else None,
                                        stats.ptr() if stats is not None else None,
@@ -272,35 +286,43 @@ def classify_bezier(coeffs, flags=None, stats: Stats | None = None, stream=None)
     n = coeffs.shape[1]
     if flags is None:
         flags = torch.empty(n, dtype=torch.uint8, device=coeffs.device)
-    _require(flags, torch.uint8, "flags")
+    _require(flags, torch.uint8, "flags", shape=(n,))
     rc = lib().hexval_classify_bezier(coeffs.data_ptr(), n, flags.data_ptr(),
                                       stats.ptr() if stats is not None else None, _stream_handle(stream))
     _check(rc, "hexval_classify_bezier")
     return flags
 
 
-def _host_array(a, dtype, name):
-    """numpy array or (pinned) CPU tensor -> (pointer, keepalive)."""
+def _host_array(a, dtype, name, shape=None):
+    """numpy array or (pinned) CPU tensor -> (pointer, keepalive); `shape` (None entries: any)."""
     if isinstance(a, np.ndarray):
         if a.dtype != dtype or not a.flags["C_CONTIGUOUS"]:
             raise TypeError(f"{name} must be a C-contiguous {dtype} array")
-        return a.ctypes.data, a
-    torch = _torch()
-    if isinstance(a, torch.Tensor):
+        ptr = a.ctypes.data
+    else:
+        torch = _torch()
+        if not isinstance(a, torch.Tensor):
+            raise TypeError(f"{name}: unsupported type {type(a)}")
         if a.is_cuda or not a.is_contiguous():
             raise TypeError(f"{name} must be a contiguous CPU tensor")
-        return a.data_ptr(), a
-    raise TypeError(f"{name}: unsupported type {type(a)}")
+        if a.element_size() != np.dtype(dtype).itemsize or a.dtype.is_floating_point != (np.dtype(dtype).kind == "f"):
+            raise TypeError(f"{name} must hold {np.dtype(dtype)} elements")
+        ptr = a.data_ptr()
+    if shape is not None:
+        got = tuple(a.shape)
+        if len(got) != len(shape) or any(w is not None and g != w for g, w in zip(got, shape)):
+            raise ValueError(f"{name} must have shape {shape}, got {got}")
+    return ptr, a
 
 
 def check_soa_host(coords, flags, coeffs=None, chunk_hexes: int = 0, stream=None):
     """hexval_check_soa_host: host (24, n) float64 in, host flags (and coeffs) out; synchronous."""
-    cp, _k1 = _host_array(coords, np.float64, "coords")
-    fp, _k2 = _host_array(flags, np.uint8, "flags")
+    cp, _k1 = _host_array(coords, np.float64, "coords", (24, None))
+    n = coords.shape[1]
+    fp, _k2 = _host_array(flags, np.uint8, "flags", (n,))
     kp = None
     if coeffs is not None:
-        kp, _k3 = _host_array(coeffs, np.float64, "coeffs")
-    n = coords.shape[1]
+        kp, _k3 = _host_array(coeffs, np.float64, "coeffs", (27, n))
     rc = lib().hexval_check_soa_host(cp, n, fp, kp, int(chunk_hexes),
                                      _stream_handle(stream) if stream is not None else 0)
     _check(rc, "hexval_check_soa_host")
@@ -308,14 +330,14 @@ def check_soa_host(coords, flags, coeffs=None, chunk_hexes: int = 0, stream=None
 
 
 def check_indexed_host(vertices, hex_idx, flags, coeffs=None, chunk_hexes: int = 0, stream=None):
-    vp, _k1 = _host_array(vertices, np.float64, "vertices")
-    ip, _k2 = _host_array(hex_idx, np.int32, "hex_idx")
-    fp, _k3 = _host_array(flags, np.uint8, "flags")
-    kp = None
-    if coeffs is not None:
-        kp, _k4 = _host_array(coeffs, np.float64, "coeffs")
+    vp, _k1 = _host_array(vertices, np.float64, "vertices", (None, 3))
+    ip, _k2 = _host_array(hex_idx, np.int32, "hex_idx", (None, 8))
     nv = vertices.shape[0]
     n = hex_idx.shape[0]
+    fp, _k3 = _host_array(flags, np.uint8, "flags", (n,))
+    kp = None
+    if coeffs is not None:
+        kp, _k4 = _host_array(coeffs, np.float64, "coeffs", (27, n))
     rc = lib().hexval_check_indexed_host(vp, nv, ip, n, fp, kp, int(chunk_hexes),
                                          _stream_handle(stream) if stream is not None else 0)
     _check(rc, "hexval_check_indexed_host")
@@ -328,18 +350,14 @@ def _quality_outputs(n, device, sj_min, test1):
         sj_min = torch.empty(n, dtype=torch.float64, device=device)
     if test1 is None or test1 is True:
         test1 = torch.empty(n, dtype=torch.uint8, device=device)
-    _require(sj_min, torch.float64, "sj_min")
-    _require(test1, torch.uint8, "test1")
+    _require(sj_min, torch.float64, "sj_min", shape=(n,))
+    _require(test1, torch.uint8, "test1", shape=(n,))
     return sj_min, test1
 
 
 def corner_quality_soa(coords, sj_min=None, test1=None, stream=None):
     """hexval_corner_quality_soa (NEXT-2): min corner scaled Jacobian and Ushakova Test 1 per hex."""
-    torch = _torch()
-    _require(coords, torch.float64, "coords", 2)
-    if coords.shape[0] != 24:
-        raise ValueError("coords must have shape (24, n)")
-    n = coords.shape[1]
+    n = _soa_input(coords)
     sj_min, test1 = _quality_outputs(n, coords.device, sj_min, test1)
     _check(lib().hexval_corner_quality_soa(coords.data_ptr(), n, sj_min.data_ptr(), test1.data_ptr(),
                                            _stream_handle(stream)), "hexval_corner_quality_soa")
@@ -348,10 +366,7 @@ def corner_quality_soa(coords, sj_min=None, test1=None, stream=None):
 
 def corner_quality_indexed(vertices, hex_idx, sj_min=None, test1=None, stream=None):
     """hexval_corner_quality_indexed (NEXT-2) on (nv, 3) float64 vertices and (n, 8) int32 connectivity."""
-    torch = _torch()
-    _require(vertices, torch.float64, "vertices", 2)
-    _require(hex_idx, torch.int32, "hex_idx", 2)
-    n = hex_idx.shape[0]
+    n = _indexed_inputs(vertices, hex_idx)
     sj_min, test1 = _quality_outputs(n, hex_idx.device, sj_min, test1)
     _check(lib().hexval_corner_quality_indexed(vertices.data_ptr(), hex_idx.data_ptr(), n, sj_min.data_ptr(),
                                                test1.data_ptr(), _stream_handle(stream)),
@@ -364,13 +379,10 @@ def check_screen_soa(coords, flags=None, sj_min=None, test1=None, stream=None):
 
     Returns ``(flags, sj_min, test1)``, bit-identical to ``check_soa`` and ``corner_quality_soa``."""
     torch = _torch()
-    _require(coords, torch.float64, "coords", 2)
-    if coords.shape[0] != 24:
-        raise ValueError("coords must have shape (24, n)")
-    n = coords.shape[1]
+    n = _soa_input(coords)
     if flags is None:
         flags = torch.empty(n, dtype=torch.uint8, device=coords.device)
-    _require(flags, torch.uint8, "flags")
+    _require(flags, torch.uint8, "flags", shape=(n,))
     sj_min, test1 = _quality_outputs(n, coords.device, sj_min, test1)
     _check(lib().hexval_check_screen_soa(coords.data_ptr(), n, flags.data_ptr(), sj_min.data_ptr(),
                                          test1.data_ptr(), _stream_handle(stream)), "hexval_check_screen_soa")
@@ -380,14 +392,10 @@ def check_screen_soa(coords, flags=None, sj_min=None, test1=None, stream=None):
 def check_screen_indexed(vertices, hex_idx, flags=None, sj_min=None, test1=None, stream=None):
     """hexval_check_screen_indexed: ``check_indexed`` and ``corner_quality_indexed`` in one pass."""
     torch = _torch()
-    _require(vertices, torch.float64, "vertices", 2)
-    _require(hex_idx, torch.int32, "hex_idx", 2)
-    if vertices.shape[1] != 3 or hex_idx.shape[1] != 8:
-        raise ValueError("vertices must be (nv, 3) and hex_idx (n, 8)")
-    n = hex_idx.shape[0]
+    n = _indexed_inputs(vertices, hex_idx)
     if flags is None:
         flags = torch.empty(n, dtype=torch.uint8, device=hex_idx.device)
-    _require(flags, torch.uint8, "flags")
+    _require(flags, torch.uint8, "flags", shape=(n,))
     sj_min, test1 = _quality_outputs(n, hex_idx.device, sj_min, test1)
     _check(lib().hexval_check_screen_indexed(vertices.data_ptr(), hex_idx.data_ptr(), n, flags.data_ptr(),
                                              sj_min.data_ptr(), test1.data_ptr(), _stream_handle(stream)),
@@ -400,38 +408,41 @@ def _bounds_outputs(n, device, lower, upper, status):
     lower = torch.empty(n, dtype=torch.float64, device=device) if lower is None else lower
     upper = torch.empty(n, dtype=torch.float64, device=device) if upper is None else upper
     status = torch.empty(n, dtype=torch.uint8, device=device) if status is None else status
-    _require(lower, torch.float64, "lower")
-    _require(upper, torch.float64, "upper")
-    _require(status, torch.uint8, "status")
+    _require(lower, torch.float64, "lower", shape=(n,))
+    _require(upper, torch.float64, "upper", shape=(n,))
+    _require(status, torch.uint8, "status", shape=(n,))
     return lower, upper, status
+
+
+def _nodes_counter(nodes):
+    if nodes is None:
+        return None
+    torch = _torch()
+    _require(nodes, torch.int64, "nodes")
+    if nodes.numel() < 1:
+        raise ValueError("nodes must hold at least one int64")
+    return nodes.data_ptr()
 
 
 def min_detj_bounds_soa(coords, rel_tol: float, lower=None, upper=None, status=None, nodes=None, stream=None):
     """hexval_min_detj_bounds_soa (NEXT-1): certified [lower, upper] on min det J per hex.
 
     ``nodes``: optional int64 CUDA tensor of one element to which the split count is added."""
-    torch = _torch()
-    _require(coords, torch.float64, "coords", 2)
-    if coords.shape[0] != 24:
-        raise ValueError("coords must have shape (24, n)")
-    n = coords.shape[1]
+    n = _soa_input(coords)
     lower, upper, status = _bounds_outputs(n, coords.device, lower, upper, status)
     _check(lib().hexval_min_detj_bounds_soa(coords.data_ptr(), n, float(rel_tol), lower.data_ptr(), upper.data_ptr(),
-                                            status.data_ptr(), nodes.data_ptr() if nodes is not None else None,
+                                            status.data_ptr(), _nodes_counter(nodes),
                                             _stream_handle(stream)), "hexval_min_detj_bounds_soa")
     return lower, upper, status
 
 
 def min_detj_bounds_indexed(vertices, hex_idx, rel_tol: float, lower=None, upper=None, status=None, nodes=None,
                             stream=None):
-    torch = _torch()
-    _require(vertices, torch.float64, "vertices", 2)
-    _require(hex_idx, torch.int32, "hex_idx", 2)
-    n = hex_idx.shape[0]
+    n = _indexed_inputs(vertices, hex_idx)
     lower, upper, status = _bounds_outputs(n, hex_idx.device, lower, upper, status)
     _check(lib().hexval_min_detj_bounds_indexed(vertices.data_ptr(), hex_idx.data_ptr(), n, float(rel_tol),
                                                 lower.data_ptr(), upper.data_ptr(), status.data_ptr(),
-                                                nodes.data_ptr() if nodes is not None else None,
+                                                _nodes_counter(nodes),
                                                 _stream_handle(stream)), "hexval_min_detj_bounds_indexed")
     return lower, upper, status
 
@@ -441,17 +452,17 @@ def select_valid(flags, group=None, n_groups: int = 0, ids=None, group_counts=No
 
     ``count`` is read back to the host (one 8-byte D2H copy) to size the ids view."""
     torch = _torch()
-    _require(flags, torch.uint8, "flags")
+    _require(flags, torch.uint8, "flags", 1)
     n = flags.numel()
     if ids is None:
         ids = torch.empty(n, dtype=torch.int32, device=flags.device)
-    _require(ids, torch.int32, "ids")
+    _require(ids, torch.int32, "ids", shape=(n,))
     count = torch.zeros(1, dtype=torch.int64, device=flags.device)
     if group is not None:
-        _require(group, torch.int32, "group")
+        _require(group, torch.int32, "group", shape=(n,))
         if group_counts is None:
             group_counts = torch.zeros(n_groups, dtype=torch.int32, device=flags.device)
-        _require(group_counts, torch.int32, "group_counts")
+        _require(group_counts, torch.int32, "group_counts", shape=(int(n_groups),))
     _check(lib().hexval_select_valid(flags.data_ptr(), n, group.data_ptr() if group is not None else None,
                                      int(n_groups), ids.data_ptr(), count.data_ptr(),
                                      group_counts.data_ptr() if group is not None else None,
@@ -465,19 +476,16 @@ def check_quad_soa(coords, flags=None, J=None, stream=None):
 
     Returns ``(flags, J)``; ``J`` is a (4, n) tensor of corner values when requested."""
     torch = _torch()
-    _require(coords, torch.float64, "coords", 2)
-    if coords.shape[0] != 8:
-        raise ValueError("coords must have shape (8, n)")
-    n = coords.shape[1]
+    n = _soa_input(coords, 8)
     if flags is None:
         flags = torch.empty(n, dtype=torch.uint8, device=coords.device)
-    _require(flags, torch.uint8, "flags")
+    _require(flags, torch.uint8, "flags", shape=(n,))
     if J is True:
         J = torch.empty((4, n), dtype=torch.float64, device=coords.device)
     elif J is False:
         J = None
     if J is not None:
-        _require(J, torch.float64, "J")
+        _require(J, torch.float64, "J", shape=(4, n))
     _check(lib().hexval_check_quad_soa(coords.data_ptr(), n, flags.data_ptr(), J.data_ptr() if J is not None else None,
                                        _stream_handle(stream)), "hexval_check_quad_soa")
     return flags, J

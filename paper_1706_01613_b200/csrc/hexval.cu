@@ -774,48 +774,57 @@ __device__ __noinline__ uint8_t exact_resolve(const double* X) {
 // K4: recursive_subdivision, depth-first per thread
 // ---------------------------------------------------------------------------
 // Warp-cooperative design: each warp owns a batch of up to 32 queued hexes
-// and a node stack in global memory (L2-resident in practice).  Every step the
-// 32 lanes split up to 32 nodes of the same depth (the top level of the
-// stack) into their 8 children (de Casteljau at t = 1/2 per axis, reading
-// G3), classify each child and push the undecided ones
-// with a warp prefix sum.  Only nodes of one depth are popped per step and
-// their children are pushed on top, so the stack is sorted by depth and holds
-// at most 32 x 8 = 256 nodes per level: K4_CAP = 19 x 256 nodes (levels
-// 1..19; children at depth 20 are classified but never pushed, reading G5).
-// Per-hex state (INVALID / depth cap reached) lives in shared memory; nodes of
-// a hex already found INVALID are dropped (the paper's early return).
+// and a node stack in global memory.  Every step the 32 lanes split up to 32
+// nodes of the same depth (the top level of the stack) into their 8 children
+// (de Casteljau at t = 1/2 per axis, reading G3), classify each child
+// and push the undecided ones with a warp prefix sum.
+// Only nodes of one depth are popped per step and their children are pushed on
+// top, so the stack is sorted by depth and holds at most 32 x 8 = 256 nodes per
+// level: K4_CAP = 19 x 256 nodes (levels 1..19; children at depth 20 are
+// classified but never pushed, reading G5).  Per-hex state (INVALID / depth
+// cap reached) lives in shared memory; nodes of a hex already found INVALID
+// are dropped (the paper's early return).
 constexpr int K4_WARPS = K4_THREADS / 32;
 constexpr int K4_CAP = (MAX_DEPTH - 1) * 256;
 
 struct WarpStacks {
-    double* coef;           // [warp][14][K4_CAP] double2: coefficient pairs (2p, 2p+1) of layout i + 3j + 9k,
-                            // the last pair's second half holding the owner (batch slot of the node's hex)
+    double* coef;           // [warp][7][K4_CAP][4]: 32-byte vectors of a node's 28 values (27 coefficients
+                            // in layout i + 3j + 9k, then the node's meta word)
 };
 
-// A node on the stack: 14 16-byte vectors per slot, the 28th value carrying
-// the node's owner (batch slot of its hex), so a push or a pop is 14 vector
-// accesses, coalesced over the warp's slots.
-__device__ __forceinline__ int stack_load(const double* sc, int slot, double* P) {
-    const double2* s2 = reinterpret_cast<const double2*>(sc);
-    int owner = 0;
-#pragma unroll
-    for (int q = 0; q < 14; ++q) {
-        const double2 v = s2[(size_t)q * K4_CAP + slot];
-        P[2 * q] = v.x;
-        if (2 * q + 1 < 27) P[2 * q + 1] = v.y;
-        else owner = __double2loint(v.y);
-    }
-    return owner;
+// 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256): a node is 7 of them.
+__device__ __forceinline__ void ld_v4(const double* p, double& a, double& b, double& c, double& d) {
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p) : "memory");
 }
-__device__ __forceinline__ void stack_store(double* sc, int slot, const double* C, int owner) {
-    double2* s2 = reinterpret_cast<double2*>(sc);
+__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+// A node on the stack: 7 x 32-byte vectors per slot, coalesced over the warp's
+// consecutive slots; value 27 is the meta word (low half: owner = batch slot of
+// the node's hex; high half: the node's scale pattern, see SplitScale).
+__device__ __forceinline__ unsigned long long stack_load(const double* sc, int slot, double* P) {
+    double m;
 #pragma unroll
-    for (int q = 0; q < 14; ++q)
-        s2[(size_t)q * K4_CAP + slot] = make_double2(C[2 * q], 2 * q + 1 < 27 ? C[2 * q + 1] : __hiloint2double(0, owner));
+    for (int q = 0; q < 7; ++q) {
+        const double* src = sc + ((size_t)q * K4_CAP + slot) * 4;
+        if (q < 6) ld_v4(src, P[4 * q], P[4 * q + 1], P[4 * q + 2], P[4 * q + 3]);
+        else ld_v4(src, P[24], P[25], P[26], m);
+    }
+    return (unsigned long long)__double_as_longlong(m);
+}
+__device__ __forceinline__ void stack_store(double* sc, int slot, const double* C, unsigned long long meta) {
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+        double* dst = sc + ((size_t)q * K4_CAP + slot) * 4;
+        if (q < 6) st_v4(dst, C[4 * q], C[4 * q + 1], C[4 * q + 2], C[4 * q + 3]);
+        else st_v4(dst, C[24], C[25], C[26], __longlong_as_double((long long)meta));
+    }
 }
 
 // One line (p0, p1, p2) split at t = 1/2: m01 = (p0+p1)/2, m = (p0+2p1+p2)/4,
-// m12 = (p1+p2)/2 (A.4 of SURVEY.md; 1 DMUL + 4 DFMA).
+// m12 = (p1+p2)/2 (A.4 of SURVEY.md; 1 DMUL + 4 DFMA).  True values: used by
+// the NEXT-1 bounds kernel, whose decisions compare coefficients with a bound.
 __device__ __forceinline__ void line_split(double p0, double p1, double p2, double& m01, double& m, double& m12) {
     const double h1 = __dmul_rn(0.5, p1);
     m01 = __fma_rn(0.5, p0, h1);
@@ -863,6 +872,91 @@ __device__ __forceinline__ void split_quarter(const double* G1, int hx, int hy, 
     }
 }
 
+// ---- K4's de Casteljau on power-of-two scaled values -----------------------
+// The validity decisions only use signs, so K4 keeps each node's coefficients
+// scaled by positive powers of two and splits a line with 3 FP64 instructions
+// instead of 5.  Scales are separable: the value at (i, j, k) is the true value
+// times s_x(i) s_y(j) s_z(k), and per axis only the ratios r01 = s(1)/s(0) and
+// r21 = s(1)/s(2) (powers of two) are needed:
+//   s01 = fma(r01, p0, p1) = s(1) (P0 + P1)      [= 2 s(1) * oracle's m01 exactly]
+//   s12 = fma(r21, p2, p1) = s(1) (P1 + P2)
+//   s   = s01 + s12        = 2 s(1) (m01 + m12)  [= 4 s(1) * oracle's m exactly]
+// (P = true values).  Because r*p is exact and a power-of-two scaling commutes
+// with rounding, every value is bit for bit the oracle's de Casteljau value
+// (oracle.c oracle_subdivide: m01 = (p0+p1)/2, m = (m01+m12)/2) times its scale
+// -- K4 makes the same decisions as the oracle's recursion on the same root.
+// The five split positions carry scales (s0, 2s1, 4s1, 2s1, s2): the left child
+// keeps (s0, 2s1, 4s1), i.e. r01' = 2 r01, r21' = 1/2; the right child
+// (4s1, 2s1, s2): r01' = 1/2, r21' = 2 r21.  A ratio exponent e >= -1 grows by
+// at most one per level, and a scale by at most 4x per axis and level (2^120
+// over 20 levels; roots are normalised, see CoordRoot).  Pattern word: six
+// 5-bit fields f = e + 1 (r01, r21 for x, y, z); the root's is all ones.
+constexpr unsigned ROOT_PATTERN = 0x02108421u;
+
+__device__ __forceinline__ double pow2_field(unsigned f) {      // 2^(f-1), f in [0, 31]
+    return __hiloint2double((int)((1022u + f) << 20), 0);
+}
+
+struct SplitScale {
+    double r01[3], r21[3];   // per axis x, y, z
+    unsigned lo[3], hi[3];   // child pattern fields per axis: left child (f01+1, 0), right child (0, f21+1), packed
+    __device__ __forceinline__ void unpack(unsigned pat) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const unsigned f01 = (pat >> (10 * a)) & 31u, f21 = (pat >> (10 * a + 5)) & 31u;
+            r01[a] = pow2_field(f01);
+            r21[a] = pow2_field(f21);
+            lo[a] = (f01 + 1u) << (10 * a);
+            hi[a] = (f21 + 1u) << (10 * a + 5);
+        }
+    }
+    __device__ __forceinline__ unsigned child(int hx, int hy, int hz) const {
+        return (hx ? hi[0] : lo[0]) | (hy ? hi[1] : lo[1]) | (hz ? hi[2] : lo[2]);
+    }
+};
+
+__device__ __forceinline__ void line_split_s(double p0, double p1, double p2, double r01, double r21, double& s01,
+                                             double& sm, double& s12) {
+    s01 = __fma_rn(r01, p0, p1);
+    s12 = __fma_rn(r21, p2, p1);
+    sm = __dadd_rn(s01, s12);
+}
+
+__device__ __forceinline__ void split_xi_s(const double* P, const SplitScale& sc, double* G1) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const double p0 = P[3 * j + 9 * k], p1 = P[1 + 3 * j + 9 * k], p2 = P[2 + 3 * j + 9 * k];
+            double s01, sm, s12;
+            line_split_s(p0, p1, p2, sc.r01[0], sc.r21[0], s01, sm, s12);
+            double* g = G1 + 5 * j + 15 * k;
+            g[0] = p0; g[1] = s01; g[2] = sm; g[3] = s12; g[4] = p2;
+        }
+}
+
+__device__ __forceinline__ void split_quarter_s(const double* G1, int hx, int hy, const SplitScale& sc, double* Z) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double B[9];                                     // B[u + 3k]: eta half hy of column a
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double* g = G1 + 2 * hx + a + 15 * k;
+            double s01, sm, s12;
+            line_split_s(g[0], g[5], g[10], sc.r01[1], sc.r21[1], s01, sm, s12);
+            if (hy == 0) { B[3 * k] = g[0]; B[1 + 3 * k] = s01; B[2 + 3 * k] = sm; }
+            else { B[3 * k] = sm; B[1 + 3 * k] = s12; B[2 + 3 * k] = g[10]; }
+        }
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            double s01, sm, s12;
+            line_split_s(B[u], B[u + 3], B[u + 6], sc.r01[2], sc.r21[2], s01, sm, s12);
+            double* z = Z + a + 3 * u;
+            z[0] = B[u]; z[9] = s01; z[18] = sm; z[27] = s12; z[36] = B[u + 6];
+        }
+    }
+}
+
 struct K4Warp {
     unsigned status[32];    // per batch slot: bit 0 INVALID found, bit 1 depth cap reached
     uint32_t hex[32];       // hex id of each batch slot
@@ -870,13 +964,22 @@ struct K4Warp {
 };
 
 // Root coefficients of queued item h: recomputed from the coordinates with
-// the pass-1 arithmetic (bit-identical), or read from caller-supplied Bezier
-// coefficients (hexval_classify_bezier).
+// the pass-1 arithmetic, or read from caller-supplied Bezier coefficients
+// (hexval_classify_bezier).  Both are normalised by a power of two when their
+// magnitude is extreme (coordinates beyond 2^+-200, coefficients beyond
+// 2^+-896), so that the subdivision's scaled values neither overflow nor
+// lose bits to subnormals; otherwise they are bit-identical to pass 1's.
 template <class L>
 __device__ __noinline__ uint8_t exact_hex(const L ld, uint32_t h) {
     double X[24];
     ld.load(h, X);
     return face_pair_coincident(X) ? (uint8_t)HEXVAL_INVALID : exact_resolve(X);
+}
+
+// 2^-e where 2^e <= max < 2^(e+1), for a max given as its (positive) hi word
+__device__ __forceinline__ double inv_pow2_of_key(int k) {
+    const int e = (k >> 20) - 1023;                       // unbiased exponent (k normal)
+    return __hiloint2double((1023 - e) << 20, 0);
 }
 
 template <class L>
@@ -885,6 +988,14 @@ struct CoordRoot {
     __device__ __forceinline__ void operator()(uint32_t h, double* P) const {
         double X[24];
         ld.load(h, X);
+        int mk = 0;
+#pragma unroll
+        for (int p = 0; p < 24; ++p) mk = max(mk, abskey(X[p]));
+        if (mk < 0x33700000 || mk >= 0x4C700000) {                 // max|x| < 2^-200 or >= 2^200
+            const double f = mk >= 0x00100000 ? inv_pow2_of_key(mk) : 0x1p1000;
+#pragma unroll
+            for (int p = 0; p < 24; ++p) X[p] = __dmul_rn(X[p], f);
+        }
         Samples s;
         samples20(X, s);
         Coeffs t;
@@ -899,8 +1010,17 @@ struct CoeffRoot {
     const double* __restrict__ b;   // coefficient-major, b[sigma*n + h]
     int64_t n;
     __device__ __forceinline__ void operator()(uint32_t h, double* P) const {
+        int mk = 0;
 #pragma unroll
-        for (int sg = 0; sg < 27; ++sg) P[kSigmaToSlot[sg]] = __ldg(b + (int64_t)sg * n + h);
+        for (int sg = 0; sg < 27; ++sg) {
+            P[kSigmaToSlot[sg]] = __ldg(b + (int64_t)sg * n + h);
+            mk = max(mk, abskey(P[kSigmaToSlot[sg]]));
+        }
+        if (mk < 0x07F00000 || mk >= 0x77F00000) {                 // max|b| < 2^-896 or >= 2^896
+            const double f = mk >= 0x00100000 ? inv_pow2_of_key(mk) : 0x1p1000;
+#pragma unroll
+            for (int c = 0; c < 27; ++c) P[c] = __dmul_rn(P[c], f);
+        }
     }
     __device__ __forceinline__ uint8_t exact(uint32_t) const { return HEXVAL_FLAG_SUBDIVIDED; }   // no exact queue
 };
@@ -928,6 +1048,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
         double P[27];
         bool act;
         int owner = lane, d;
+        unsigned pat = ROOT_PATTERN;                     // scale pattern of the node (see SplitScale)
         if (top == 0) {
             // batch done: write its verdicts (precedence INVALID > UNDETERMINED > VALID, reading G4)
             if (lane < nb) {
@@ -978,7 +1099,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             d = 0;
             if (act) {
                 W.status[lane] = 0;
-                root(W.hex[lane], P);                    // bit-identical to pass 1
+                root(W.hex[lane], P);                    // pass 1's root (normalised if extreme)
             }
         } else {
             const int k = min(32, W.cnt[D]);
@@ -987,7 +1108,9 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             d = D;
             if (act) {
                 const int slot = top - k + lane;
-                owner = stack_load(sc, slot, P);
+                const unsigned long long meta = stack_load(sc, slot, P);
+                owner = (int)(unsigned)meta;
+                pat = (unsigned)(meta >> 32);
                 act = (W.status[owner] & 1u) == 0;       // hex already INVALID: drop the node
             }
             top -= k;
@@ -999,8 +1122,10 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
         if (STATS && actmask) { nodes += __popc(actmask); maxd = max(maxd, d + 1); }
         if (STATS) ++steps;
         // ---- split every active node into its 8 children --------------------
+        SplitScale ss;
+        ss.unpack(pat);
         double G1[45];
-        split_xi(P, G1);
+        split_xi_s(P, ss, G1);
         bool inval = false, capped = false;
         int pushed = 0;                                  // warp-uniform
         const bool can_push = d + 1 < MAX_DEPTH;
@@ -1009,22 +1134,28 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
 #pragma unroll
             for (int hy = 0; hy < 2; ++hy) {
                 double Z[45];
-                split_quarter(G1, hx, hy, Z);
-                // classify the two children (zeta halves hz = 0, 1)
+                split_quarter_s(G1, hx, hy, ss, Z);
+                // classify the two children (zeta halves hz = 0, 1) from per-plane key
+                // minima: planes v = 0, 2, 4 split into their 4 corners and 5 others,
+                // planes 1 and 3 lie inside both children
+                int pc[3], pr[3], pa[2];
+#pragma unroll
+                for (int w = 0; w < 3; ++w) {
+                    const double* z = Z + 18 * w;
+                    pc[w] = min(min(key(z[0]), key(z[2])), min(key(z[6]), key(z[8])));
+                    pr[w] = min(min(min(key(z[1]), key(z[3])), key(z[4])), min(key(z[5]), key(z[7])));
+                }
+#pragma unroll
+                for (int w = 0; w < 2; ++w) {
+                    const double* z = Z + 9 + 18 * w;
+                    pa[w] = min(min(min(key(z[0]), key(z[1])), min(key(z[2]), key(z[3]))),
+                                min(min(key(z[4]), key(z[5])), min(min(key(z[6]), key(z[7])), key(z[8]))));
+                }
                 bool push[2];
 #pragma unroll
                 for (int hz = 0; hz < 2; ++hz) {
-                    int mc = 0x7fffffff, mi = 0x7fffffff;
-#pragma unroll
-                    for (int v = 0; v < 3; ++v)
-#pragma unroll
-                        for (int u = 0; u < 3; ++u)
-#pragma unroll
-                            for (int a = 0; a < 3; ++a) {
-                                const int kk = key(Z[a + 3 * u + 9 * (2 * hz + v)]);
-                                if (a != 1 && u != 1 && v != 1) mc = min(mc, kk);
-                                else mi = min(mi, kk);
-                            }
+                    const int mc = min(pc[hz], pc[hz + 1]);
+                    const int mi = min(min(pr[hz], pr[hz + 1]), pa[hz]);
                     const bool bad = act && mc <= 0;               // a corner value <= 0: INVALID
                     const bool und = act && mc > 0 && mi <= 0;     // undecided child
                     inval |= bad;
@@ -1048,7 +1179,9 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
                                 for (int u = 0; u < 3; ++u)
 #pragma unroll
                                     for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
-                            stack_store(sc, slot, C, owner);
+                            stack_store(sc, slot, C,
+                                        (unsigned long long)(unsigned)owner |
+                                            ((unsigned long long)ss.child(hx, hy, hz) << 32));
 
                         }
                     }
@@ -1233,7 +1366,7 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
             d = D;
             if (lane < k) {
                 const int slot = top - k + lane;
-                owner = stack_load(sc, slot, P);
+                owner = (int)(unsigned)stack_load(sc, slot, P);
                 // upper may have dropped since the push: the node may now be a leaf
                 double mn = P[0];
 #pragma unroll

@@ -110,3 +110,25 @@ def test_binding_validation_without_gpu():
         hv.check_screen_indexed(torch.zeros((4, 3), dtype=torch.float64), torch.zeros((4, 8), dtype=torch.int32))
     with pytest.raises(TypeError):
         hv.check_soa_host(np.zeros((24, 3), np.float32), np.zeros(3, np.uint8))
+
+
+def test_host_call_rejects_mis_shaped_buffers_before_any_copy():
+    """check_*_host validate every host buffer's shape before the library is called: an
+    undersized flags / coeffs array or a wrongly shaped coords / connectivity array would
+    otherwise be overrun by the device-to-host copies."""
+    coords = np.zeros((24, 10))
+    with pytest.raises(ValueError):
+        hv.check_soa_host(coords, np.zeros(9, np.uint8))
+    with pytest.raises(ValueError):
+        hv.check_soa_host(np.zeros((23, 10)), np.zeros(10, np.uint8))
+    with pytest.raises(ValueError):
+        hv.check_soa_host(coords, np.zeros(10, np.uint8), coeffs=np.zeros((10, 27)))
+    with pytest.raises(TypeError):
+        hv.check_soa_host(coords, np.zeros(10, np.int32))
+    verts, idx = np.zeros((5, 3)), np.zeros((10, 8), np.int32)
+    with pytest.raises(ValueError):
+        hv.check_indexed_host(verts, np.zeros((10, 4), np.int32), np.zeros(10, np.uint8))
+    with pytest.raises(ValueError):
+        hv.check_indexed_host(np.zeros((5, 4)), idx, np.zeros(10, np.uint8))
+    with pytest.raises(ValueError):
+        hv.check_indexed_host(verts, idx, np.zeros(10, np.uint8), coeffs=np.zeros((27, 9)))

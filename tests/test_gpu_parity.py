@@ -91,6 +91,38 @@ def test_root_emulation_is_bit_exact():
     assert np.array_equal(k.view(np.uint64), emu.view(np.uint64))
 
 
+def test_binding_rejects_mis_shaped_outputs():
+    """Every caller-supplied output is checked against n before the library writes it
+    (ADVICE r1): undersized or transposed buffers raise instead of being overrun."""
+    coords = torch.from_numpy(hexgen.soa_config(100, 0.3, 5)).cuda()
+    verts, idx = hexgen.indexed_config(3, start=0, count=100)
+    v, i = torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda()
+    f99 = torch.empty(99, dtype=torch.uint8, device="cuda")
+    d99 = torch.empty(99, dtype=torch.float64, device="cuda")
+    bad = [
+        lambda: hv.check_soa(coords, flags=f99),
+        lambda: hv.check_soa(coords, coeffs=torch.empty((100, 27), dtype=torch.float64, device="cuda")),
+        lambda: hv.check_indexed(v, i, flags=f99),
+        lambda: hv.check_indexed(v, i[:, :4].contiguous()),
+        lambda: hv.corner_quality_indexed(v, i[:, :4].contiguous()),
+        lambda: hv.corner_quality_soa(coords, sj_min=d99),
+        lambda: hv.check_screen_soa(coords, test1=f99),
+        lambda: hv.min_detj_bounds_soa(coords, 1e-3, lower=d99),
+        lambda: hv.min_detj_bounds_indexed(v, i[:, :4].contiguous(), 1e-3),
+        lambda: hv.classify_bezier(torch.empty((27, 100), dtype=torch.float64, device="cuda"), flags=f99),
+        lambda: hv.check_quad_soa(torch.zeros((8, 100), dtype=torch.float64, device="cuda"),
+                                  J=torch.empty((4, 99), dtype=torch.float64, device="cuda")),
+        lambda: hv.select_valid(torch.zeros(100, dtype=torch.uint8, device="cuda"), ids=torch.empty(
+            99, dtype=torch.int32, device="cuda")),
+        lambda: hv.select_valid(torch.zeros(100, dtype=torch.uint8, device="cuda"),
+                                group=torch.zeros(100, dtype=torch.int32, device="cuda"), n_groups=10,
+                                group_counts=torch.zeros(9, dtype=torch.int32, device="cuda")),
+    ]
+    for k, call in enumerate(bad):
+        with pytest.raises(ValueError):
+            call()
+
+
 def test_paper_figures(golden_hexes):
     X = np.stack([golden_hexes[k][0] for k in ("fig5_invalid", "fig6_valid", "fig7_invalid")])
     coords = hexgen.nodes_to_soa(X)
@@ -406,6 +438,33 @@ def test_classify_bezier_depth_cap_and_random():
     assert np.array_equal(f, ref_flags)
     assert np.sum((f & 3) == hv.INVALID) > 100 and np.sum(f == (hv.VALID | 4)) > 100
     assert stats.read()["n_nodes"] >= nodes_full
+
+
+def test_subdivision_decisions_identical_to_the_oracle_recursion():
+    """K4 keeps power-of-two scaled coefficients whose values are bit for bit the oracle's
+    de Casteljau values (oracle_subdivide) times their scales, so from the same root it takes
+    exactly the oracle's decisions: on the oracle's own root coefficients of config-4 hexes
+    (pushed corners, twisted prisms down to |r| = 1e-5) and random hexes, hexval_classify_bezier
+    returns the oracle's flags on EVERY item (near-boundary ones included), and over the VALID
+    items exactly the oracle's number of subdivision nodes."""
+    c4, _ = hexgen.adversarial_config(6000, seed=4, start=200_000)
+    rnd = hexgen.soa_config(4000, 0.45, 77)
+    coords = np.ascontiguousarray(np.concatenate([c4, rnd], axis=1))
+    b = oracle.check_soa(coords, want_coeffs=True)["coeffs"]
+    m = b.shape[1]
+    ref = [oracle.classify_coeffs(b[:, j], 1.0) for j in range(m)]
+    ref_flags = np.array([r["flags"] for r in ref], np.uint8)
+    f = hv.classify_bezier(torch.from_numpy(b).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(f.cpu().numpy(), ref_flags)
+    sub = ref_flags & 4 != 0
+    assert sub.sum() > 2500 and ((ref_flags & 3) == 0).sum() > 1000
+    valid = np.nonzero(ref_flags == (hv.VALID | hv.FLAG_SUBDIVIDED))[0]
+    stats = hv.Stats()
+    fv = hv.classify_bezier(torch.from_numpy(np.ascontiguousarray(b[:, valid])).cuda(), stats=stats)
+    torch.cuda.synchronize()
+    assert np.all(fv.cpu().numpy() == (hv.VALID | hv.FLAG_SUBDIVIDED))
+    assert stats.read()["n_nodes"] == sum(ref[j]["nodes"] for j in valid)
 
 
 def test_indexed_equals_soa_and_host_path():
