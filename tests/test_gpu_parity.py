@@ -561,6 +561,25 @@ def test_config4_full_size_closed_form_and_sampled():
     assert_flags_match(f[sel], ref)
 
 
+def test_config4_every_hex_against_the_oracle():
+    """Config 4 (4M adversarial hexes, ~5e9 subdivision nodes) compared on EVERY hex, whole
+    flags byte (verdict and SUBDIVIDED bit), against the oracle's flags stored by
+    tools/make_config4_golden.py (which calls only oracle/; 26 min on 8 host cores).  The
+    oracle marks no hex near-boundary.  For the VALID hexes the subdivision node counts are
+    order independent (reading G4): their GPU total equals the oracle's."""
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "config4_oracle.npz"))
+    _, coords, _ = hexgen.make(4)
+    assert int(g["n"]) == coords.shape[1] and int(g["seed"]) == 4
+    assert int(g["near"].sum()) == 0
+    f, _ = gpu_soa(coords)
+    assert np.array_equal(f, g["flags"])
+    valid = np.nonzero(g["flags"] == (hv.VALID | hv.FLAG_SUBDIVIDED))[0]
+    stats = hv.Stats()
+    fv, _ = gpu_soa(np.ascontiguousarray(coords[:, valid]), stats=stats)
+    assert np.all(fv == hv.VALID | hv.FLAG_SUBDIVIDED)
+    assert stats.read()["n_nodes"] == int(g["nodes"][valid].astype(np.int64).sum())
+
+
 def test_subdivision_node_count_equals_oracle_for_valid_hexes():
     """VALID hexes explore their whole capped tree, so the number of subdivided nodes is
     order independent (reading G4): the warp-cooperative K4 must count exactly what the
