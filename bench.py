@@ -37,7 +37,10 @@ FALLBACK_HBM_GBS = 6650.0
 # fp64 operations per subdivision node: 147 new de Casteljau values, one add and one
 # multiply each; peak = 148 SMs x 64 FP64 lanes x 1.965 GHz
 FP64_OPS_PER_NODE = 294
-FP64_PEAK_GOPS = 148 * 64 * 1.965
+# fp64 operations per hex of pass 1 (36 + 36 vector components, 180 for the 20 triple
+# products, 19 Step-2 compares, ~90 for T~, 18 Step-4 compares)
+FP64_OPS_PER_HEX = 381
+FP64_PEAK_GOPS = 148 * 64 * 1.965            # datasheet-level fallback when the probe cannot run
 CONFIG_DESC = {
     0: "config0: 10k perturbed unit cubes, SoA fp64, noise U[-0.25,0.25]^3, seed 0",
     1: "config1: 10M perturbed unit cubes, SoA fp64, noise U[-0.35,0.35]^3, seed 1",
@@ -63,8 +66,16 @@ def parse():
     p.add_argument("--config", type=int, default=1, choices=sorted(CONFIG_DESC))
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--clock-ms", type=float, default=10.0,
+    p.add_argument("--clock-ms", type=float, default=0.5,
                    help="NVML clock sampling period during the timed region (ms)")
+    p.add_argument("--no-secondary", action="store_true",
+                   help="skip the secondary block (config-4 subdivision and config-3 pass 1 against the "
+                        "measured FP64 peak)")
+    p.add_argument("--dry-run", action="store_true",
+                   help="no GPU: shard ranges + oracle verdict counts on a sample of each rank's shard, summed "
+                        "over ranks (gloo); tests the multi-rank plumbing on CPU")
+    p.add_argument("--workers", type=int, default=min(16, os.cpu_count() or 1),
+                   help="host processes generating the synthetic inputs")
     p.add_argument("--no-cupti", action="store_true",
                    help="skip the torch.profiler (CUPTI) kernel-duration pass (e.g. under ncu)")
     p.add_argument("--graph", action="store_true",
@@ -183,15 +194,33 @@ def cupti_kernel_us(step, steps: int) -> dict:
     return {k: tot / c for k, (c, tot) in per.items()}, {k: c for k, (c, _) in per.items()}
 
 
-def dist_setup(gpus: int):
+def spawn_ranks(gpus: int) -> int:
+    """`bench.py --gpus N` without a process group: re-run this command under
+    torch.distributed.run with N ranks (one per GPU) on 127.0.0.1 and return its exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_setup(gpus: int, dry_run: bool = False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dry_run:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if gpus != world:
+        raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     return world, rank, local
 
 
@@ -209,21 +238,23 @@ def barrier(world: int):
 # ---------------------------------------------------------------------------
 # CPU oracle (baseline / reference arm)
 # ---------------------------------------------------------------------------
-def oracle_sample(cfg: int, m: int, start: int = 0, nthreads: int = 0):
-    import hexgen
+def oracle_sample(cfg: int, m: int, start: int = 0, nthreads: int = 0, rank: int = 0, workers: int = 1):
+    """A callable running the oracle on hexes start..start+m-1 of this rank's shard of `cfg`."""
     import oracle
-    if cfg in (0, 1):
-        coords = hexgen.soa_config(m, 0.25 if cfg == 0 else 0.35, cfg, start)
+    layout, *arrays = shard_inputs(cfg, rank, start, m, workers)
+    if layout == "soa":
+        coords = arrays[0]
         return lambda: oracle.check_soa(coords, nthreads=nthreads)
-    if cfg == 4:
-        coords, _ = hexgen.adversarial_config(m, 4, start)
-        return lambda: oracle.check_soa(coords, nthreads=nthreads)
-    _, verts, idx = hexgen.make(cfg, start, m)
+    verts, idx = arrays
     return lambda: oracle.check_indexed(verts, idx, nthreads=nthreads)
 
 
-def oracle_rate(cfg: int, seconds: float, start: int = 0):
-    """Time the oracle, as it stands, on a bounded prefix sample of the workload (all host threads)."""
+def oracle_rate(cfg: int, seconds: float, start: int = 0, gpu_flags=None, workers: int = 1):
+    """Time the oracle, as it stands, on a bounded prefix sample of the workload (all host threads).
+
+    With `gpu_flags` (the flags of a timed GPU step, host copy) the sample's oracle verdicts are also
+    compared with them: `parity` = flag mismatches on hexes the oracle does not mark near-boundary,
+    and the near-boundary count (BASELINE north_star: must be 0 on configs 0-3)."""
     import hexgen
     import oracle
     n = hexgen.config_size(cfg)
@@ -235,10 +266,18 @@ def oracle_rate(cfg: int, seconds: float, start: int = 0):
     run()
     r0 = probe_n / (time.perf_counter() - t0)
     m = int(min(n, max(probe_n, r0 * seconds)))
-    run = oracle_sample(cfg, m, start)
+    run = oracle_sample(cfg, m, start, workers=workers)
     t0 = time.perf_counter()
-    run()
+    ref = run()
     dt = time.perf_counter() - t0
+    parity = None
+    if gpu_flags is not None:
+        import numpy as np
+        g = np.asarray(gpu_flags[start:start + m])
+        near = ref["near"].astype(bool)
+        parity = {"compared": int(m), "mismatches": int(np.sum((g != ref["flags"]) & ~near)),
+                  "near_boundary": int(near.sum()),
+                  "what": "whole flags byte of the last timed GPU step vs the oracle on the same hexes"}
     # one thread on a smaller slice of the same stream (per-core rate, the unit of the
     # paper's ~6 M hex/s on one core)
     m1 = max(1000, min(m, int(m / max(1, cores) / 4)))
@@ -246,9 +285,12 @@ def oracle_rate(cfg: int, seconds: float, start: int = 0):
     t1 = time.perf_counter()
     run1()
     dt1 = time.perf_counter() - t1
-    return {"value": m / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"hexes {start}..{start + m - 1} of {CONFIG_DESC[cfg]} ({m} hexes, {dt:.2f} s wall on {cores} threads)",
-            "single_thread": {"value": m1 / dt1, "unit": UNIT, "sample": f"hexes {start}..{start + m1 - 1}, 1 thread"}}
+    out = {"value": m / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"hexes {start}..{start + m - 1} of {CONFIG_DESC[cfg]} ({m} hexes, {dt:.2f} s wall on {cores} threads)",
+           "single_thread": {"value": m1 / dt1, "unit": UNIT, "sample": f"hexes {start}..{start + m1 - 1}, 1 thread"}}
+    if parity is not None:
+        out["parity"] = parity
+    return out
 
 
 def run_reference(args, world, rank):
@@ -265,7 +307,7 @@ def run_reference(args, world, rank):
         per_step.append(last["value"])
     value = statistics.median(per_step)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIG_DESC[args.config], "n_hexes": n,
@@ -283,18 +325,37 @@ def run_reference(args, world, rank):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def make_inputs(cfg: int, rank: int):
-    """Host arrays of this rank's shard (weak scaling: every rank its own n hexes)."""
+def shard_inputs(cfg: int, rank: int, offset: int = 0, count: int | None = None, workers: int = 1):
+    """(layout, *arrays) of hexes offset..offset+count-1 of rank `rank`'s weak-scaling shard.
+
+    Every rank gets its own, distinct hexes of the configuration's family:
+    configs 0, 1, 4: the synthetic hexes r*n .. r*n+n-1 of the stream; config 3: candidates
+    r*n .. r*n+n-1 of the candidate stream on the shared 100^3 grid (the 24 MB vertex array is
+    replicated); config 2: the k-slab r of a 200 x 200 x 200N structured grid (its own 201^3
+    vertices, boundary plane shared with slab r-1)."""
     import hexgen
     from paper_1706_01613_b200 import shard
     start, n = shard.weak_shard(hexgen.config_size(cfg), rank)
-    if cfg in (0, 1):
-        return "soa", n, (hexgen.soa_config(n, 0.25 if cfg == 0 else 0.35, cfg, start=start),)
-    if cfg == 4:
-        coords, _ = hexgen.adversarial_config(n, 4, start=start)
-        return "soa", n, (coords,)
-    _, verts, idx = hexgen.make(cfg)
-    return "indexed", n, (verts, idx)
+    count = n - offset if count is None else count
+    if cfg == 2:
+        return ("indexed", *hexgen.indexed_config(2, start=offset, count=count, slab=rank))
+    out = hexgen.make(cfg, start=start + offset, count=count, workers=workers)
+    return ("soa", out[1]) if out[0] == "soa" else ("indexed", out[1], out[2])
+
+
+def shard_range(cfg: int, rank: int) -> tuple[int, int]:
+    """[first, last) global hex index of rank `rank`'s shard (config 2: global cell ids of its k-slab)."""
+    import hexgen
+    from paper_1706_01613_b200 import shard
+    start, n = shard.weak_shard(hexgen.config_size(cfg), rank)
+    return start, start + n
+
+
+def make_inputs(cfg: int, rank: int, workers: int = 1):
+    """Host arrays of this rank's shard (weak scaling: every rank its own n hexes)."""
+    layout, *arrays = shard_inputs(cfg, rank, workers=workers)
+    n = arrays[0].shape[1] if layout == "soa" else arrays[1].shape[0]
+    return layout, n, tuple(arrays)
 
 
 def algorithmic_bytes(layout: str, n: int, arrays, coeffs: bool = False) -> int:
@@ -315,7 +376,7 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     cfg = args.config
     desc = CONFIG_DESC[cfg]
-    layout, n, host = make_inputs(cfg, rank)
+    layout, n, host = make_inputs(cfg, rank, args.workers)
     dev = [torch.from_numpy(a).cuda() for a in host]
     flags = torch.empty(n, dtype=torch.uint8, device="cuda")
     coeffs = torch.empty((27, n), dtype=torch.float64, device="cuda") if args.coeffs else None
@@ -355,6 +416,7 @@ def run_ours(args, world, rank, local):
         barrier(world)
     ms_total = ev0.elapsed_time(ev1)
     ms_step = dist_max(ms_total / args.steps, world)
+    flags_timed = flags.cpu().numpy() if rank == 0 and world == 1 and not args.no_cpu_baseline else None
     graph = None
     if args.graph:
         # the same call captured once in a CUDA graph and replayed K times
@@ -513,9 +575,15 @@ def run_ours(args, world, rank, local):
         if not torch.equal(flags.cpu(), fl_h):
             e2e["warning"] = "host-path flags differ from device-path flags"
 
+    secondary = None
+    if world == 1 and not args.no_secondary:
+        del flags
+        torch.cuda.empty_cache()
+        secondary = run_secondary(args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_rate(cfg, args.cpu_seconds)
+        cpu = oracle_rate(cfg, args.cpu_seconds, gpu_flags=flags_timed, workers=args.workers)
 
     if rank == 0:
         line = {
@@ -523,7 +591,8 @@ def run_ours(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "n_hexes_per_rank": n, "global_hexes": world * n, "layout": layout,
-                       "parallelism": f"independent shards x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"independent shards x{world} (weak scaling; multi-GPU unmeasured on hardware until a "
+                            "driver SCALE run)") if world > 1 else "single GPU",
                        "l2": L2_NOTE[cfg],
                        "pass1_variant": os.environ.get("HEXVAL_PASS1", "default"),
                        "coefficients_written": bool(args.coeffs)},
@@ -533,6 +602,7 @@ def run_ours(args, world, rank, local):
             "gpu_launches": hv.kernel_launches_per_call() * args.steps,
             "clocks": clk.summary(),
             "subdivision": subdivision,
+            **({"secondary": secondary} if secondary else {}),
             **({"graph": graph} if graph else {}),
             "subdivision_rate": st["n_subdivided"] / (world * n),
             "verdicts": {"valid": st["n_valid"], "invalid": st["n_invalid"],
@@ -543,6 +613,63 @@ def run_ours(args, world, rank, local):
         }
         print(json.dumps(line), flush=True)
     return 0
+
+
+def run_secondary(args):
+    """The FP64-bound kernels of the path against a MEASURED FP64 peak (DFMA probe, same process):
+    the subdivision kernel on config 4 (4M adversarial hexes, ~5e9 nodes) and indexed pass 1 on
+    config 3 (40M candidates).  Kernel durations from CUPTI activity records; algorithmic FP64
+    operations per unit from SURVEY.md 8(d) (294 per subdivision node, 381 per pass-1 hex)."""
+    import torch
+
+    import paper_1706_01613_b200 as hv
+    out = {}
+    try:
+        pk = hv.fp64_peak()
+        peak, src = pk["dfma_per_s"], ("measured: hexval_diag_fp64_peak, DFMA-only kernel, 8 chains/thread, "
+                                        "8x256 threads/SM, best of 5 launches, DFMA lane-instructions/s")
+    except Exception as exc:                                          # probe unavailable: datasheet level
+        peak, src = FP64_PEAK_GOPS * 1e9, f"fallback 148 SMs x 64 lanes x 1.965 GHz ({str(exc)[:80]})"
+    out["fp64_peak"] = {"value": peak, "unit": "FP64 lane-instr/s", "source": src}
+    # config 4: subdivision
+    layout, n4, host4 = make_inputs(4, 0, args.workers)
+    c4 = torch.from_numpy(host4[0]).cuda()
+    fl4 = torch.empty(n4, dtype=torch.uint8, device="cuda")
+    st = hv.Stats()
+    hv.check_soa(c4, flags=fl4, stats=st)
+    torch.cuda.synchronize()
+    st = st.read()
+    ksteps = 3
+    kern, _ = cupti_kernel_us(lambda: hv.check_soa(c4, flags=fl4), ksteps)
+    k4_s = kern.get("subdiv_kernel", float("nan")) * 1e-6
+    out["config4_subdivision"] = {
+        "workload": CONFIG_DESC[4], "kernel": "subdiv_kernel (K4)", "kernel_ms": k4_s * 1e3,
+        "pass1_ms": kern.get("soa_cp_kernel", float("nan")) * 1e-3,
+        "nodes": st["n_nodes"], "subdivided_hexes": st["n_subdivided"], "max_depth": st["max_depth"],
+        "nodes_per_s": st["n_nodes"] / k4_s, "lane_use": st["n_nodes"] / max(1, st["n_lane_steps"]),
+        "fp64_ops_per_node": FP64_OPS_PER_NODE,
+        "fp64_achieved": st["n_nodes"] * FP64_OPS_PER_NODE / k4_s,
+        "frac": st["n_nodes"] * FP64_OPS_PER_NODE / k4_s / peak,
+        "timing": f"mean CUPTI kernel duration over {ksteps} calls"}
+    del c4, fl4
+    torch.cuda.empty_cache()
+    # config 3: indexed pass 1
+    layout, n3, host3 = make_inputs(3, 0, args.workers)
+    v3, i3 = (torch.from_numpy(a).cuda() for a in host3)
+    fl3 = torch.empty(n3, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        hv.check_indexed(v3, i3, flags=fl3)
+    ksteps = 10
+    kern, _ = cupti_kernel_us(lambda: hv.check_indexed(v3, i3, flags=fl3), ksteps)
+    p1_s = next((v for k, v in kern.items() if k in ("idx_cp_kernel", "plain_kernel")), float("nan")) * 1e-6
+    out["config3_pass1"] = {
+        "workload": CONFIG_DESC[3], "kernel": "idx_cp_kernel (K2)", "kernel_ms": p1_s * 1e3,
+        "hexes_per_s": n3 / p1_s, "fp64_ops_per_hex": FP64_OPS_PER_HEX,
+        "fp64_achieved": n3 * FP64_OPS_PER_HEX / p1_s, "frac": n3 * FP64_OPS_PER_HEX / p1_s / peak,
+        "timing": f"mean CUPTI kernel duration over {ksteps} calls"}
+    del v3, i3, fl3
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_op(args, world, rank, local):
@@ -560,7 +687,7 @@ def run_op(args, world, rank, local):
         start, n = shard.weak_shard(10_000_000, rank)
         layout, host = "quad-soa", (hexgen.quad_soa(n, 0.35, 5, start),)
     else:
-        layout, n, host = make_inputs(cfg, rank)
+        layout, n, host = make_inputs(cfg, rank, args.workers)
     dev = [torch.from_numpy(a).cuda() for a in host]
     stream = torch.cuda.current_stream()
     in_bytes = None
@@ -679,10 +806,41 @@ def run_op(args, world, rank, local):
     return 0
 
 
+def run_dry(args, world, rank):
+    """CPU-only check of the multi-rank plumbing (tests/test_shard.py): every rank reports its shard
+    range and runs the oracle on the first hexes of its shard; the verdict counts are summed with the
+    same collective the GPU run uses."""
+    import numpy as np
+
+    from paper_1706_01613_b200 import shard
+    m = 2000
+    ref = oracle_sample(args.config, m, 0, nthreads=1, rank=rank)()
+    counts = np.bincount(ref["flags"] & 3, minlength=4).tolist()
+    summed = shard.sum_over_ranks(counts)
+    lo, hi = shard_range(args.config, rank)
+    layout, *arrays = shard_inputs(args.config, rank, 0, 4)
+    first = float(arrays[0].ravel()[0]) if layout == "soa" else float(arrays[0][arrays[1][0, 0], 2])
+    ranges = [None] * world
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_gather_object(ranges, {"rank": rank, "range": [lo, hi], "first_coord": first})
+    else:
+        ranges = [{"rank": rank, "range": [lo, hi], "first_coord": first}]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "world": world, "config": args.config, "shards": ranges,
+                          "sample_per_rank": m, "verdicts_summed": dict(zip(["invalid", "valid", "undetermined",
+                                                                              "nonfinite"], summed))}), flush=True)
+    return 0
+
+
 def main():
     args = parse()
-    world, rank, local = dist_setup(args.gpus)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)                 # one process per GPU, launched for the caller
+    world, rank, local = dist_setup(args.gpus, args.dry_run)
     try:
+        if args.dry_run:
+            return run_dry(args, world, rank)
         if args.impl == "reference":
             return run_reference(args, world, rank)
         if args.op != "check":

@@ -97,16 +97,21 @@ def soa_config(n: int, amp: float, seed: int, start: int = 0) -> np.ndarray:
 # configs 2 / 3: jittered structured grid + connectivity
 # --------------------------------------------------------------------------
 
-def grid_vertices(m: int, jitter: float, seed: int) -> np.ndarray:
-    """(m^3, 3) vertices; id = i + m*(j + m*k) sits at (i, j, k) + U[-jitter, jitter]^3."""
+def grid_vertices(m: int, jitter: float, seed: int, k0: int = 0) -> np.ndarray:
+    """(m^3, 3) vertices; id = i + m*(j + m*k) sits at (i, j, k + k0) + U[-jitter, jitter]^3.
+
+    ``k0`` shifts the block along k (weak-scaling shards of config 2: rank r takes the
+    k-slab starting at plane 200 r of a 200 x 200 x 200N grid); the jitter is drawn at the
+    vertex's global id, so neighbouring slabs share their boundary plane exactly."""
     nv = m ** 3
     ids = np.arange(nv, dtype=np.uint64)
     i = (ids % np.uint64(m)).astype(np.float64)
     j = ((ids // np.uint64(m)) % np.uint64(m)).astype(np.float64)
-    k = (ids // np.uint64(m * m)).astype(np.float64)
+    kk = ids // np.uint64(m * m) + np.uint64(k0)
+    gid = ids + np.uint64(k0 * m * m)
     v = np.empty((nv, 3), dtype=np.float64)
-    for a, base in enumerate((i, j, k)):
-        v[:, a] = base + jitter * (2.0 * uniform(seed, 1000 + a, ids) - 1.0)
+    for a, base in enumerate((i, j, kk.astype(np.float64))):
+        v[:, a] = base + jitter * (2.0 * uniform(seed, 1000 + a, gid) - 1.0)
     return v
 
 
@@ -167,11 +172,15 @@ def candidate_connectivity(m: int, n: int, p_swap: float, seed: int, start: int 
     return conn.astype(np.int32)
 
 
-def indexed_config(cfg: int, start: int = 0, count: int | None = None):
-    """(vertices, hex_idx) for config 2 (structured 200^3) or 3 (40M candidates)."""
+def indexed_config(cfg: int, start: int = 0, count: int | None = None, slab: int = 0, workers: int = 1):
+    """(vertices, hex_idx) for config 2 (structured 200^3) or 3 (40M candidates).
+
+    ``slab`` (config 2): the k-slab ``slab`` of a grid stacked along k (see grid_vertices).
+    ``workers`` > 1 generates config 3's connectivity in parallel chunks (identical result:
+    every draw is addressed by the candidate id)."""
     if cfg == 2:
         m, jit, seed, n_total = 201, 0.3, 2, 200 ** 3
-        verts = grid_vertices(m, jit, seed)
+        verts = grid_vertices(m, jit, seed, k0=200 * slab)
         n = n_total - start if count is None else count
         cells = np.arange(start, start + n, dtype=np.int64)
         return verts, cell_connectivity(m, cells).astype(np.int32)
@@ -179,8 +188,32 @@ def indexed_config(cfg: int, start: int = 0, count: int | None = None):
         m, jit, seed, n_total = 100, 0.2, 3, 40_000_000
         verts = grid_vertices(m, jit, seed)
         n = n_total - start if count is None else count
-        return verts, candidate_connectivity(m, n, 0.1, seed, start)
+        return verts, _chunked(lambda a, c: candidate_connectivity(m, c, 0.1, seed, a), start, n, workers, axis=0)
     raise ValueError(cfg)
+
+
+def _chunked(fn, start: int, n: int, workers: int, axis: int):
+    """fn(start, count) over ``workers`` contiguous chunks in forked processes, concatenated."""
+    if workers <= 1 or n < 2_000_000:
+        return fn(start, n)
+    import multiprocessing as mp
+    global _FORK_FN
+    step = -(-n // workers)
+    parts = [(a, min(step, start + n - a)) for a in range(start, start + n, step)]
+    _FORK_FN = fn                                   # inherited by the forked workers
+    try:
+        with mp.get_context("fork").Pool(len(parts)) as pool:
+            out = pool.map(_fork_call, parts)
+    finally:
+        _FORK_FN = None
+    return np.ascontiguousarray(np.concatenate(out, axis=axis))
+
+
+_FORK_FN = None
+
+
+def _fork_call(ac):
+    return _FORK_FN(*ac)
 
 
 # --------------------------------------------------------------------------
@@ -381,20 +414,21 @@ def config_size(cfg: int) -> int:
     return CONFIGS[cfg].n
 
 
-def make(cfg: int, start: int = 0, count: int | None = None):
+def make(cfg: int, start: int = 0, count: int | None = None, workers: int = 1, slab: int = 0):
     """Generate (part of) a configuration.
 
     Returns ``("soa", coords)`` / ``("soa", coords, r)`` for configs 0, 1, 4 and
-    ``("indexed", vertices, hex_idx)`` for configs 2, 3.
+    ``("indexed", vertices, hex_idx)`` for configs 2, 3.  ``workers`` > 1 generates large
+    configurations in parallel chunks (bit-identical to the serial result).
     """
     info = CONFIGS[cfg]
     n = info.n - start if count is None else count
     if cfg == 0:
         return ("soa", soa_config(n, 0.25, 0, start))
     if cfg == 1:
-        return ("soa", soa_config(n, 0.35, 1, start))
+        return ("soa", _chunked(lambda a, c: soa_config(c, 0.35, 1, a), start, n, workers, axis=1))
     if cfg == 4:
-        coords, r = adversarial_config(n, 4, start)
-        return ("soa", coords, r)
-    verts, idx = indexed_config(cfg, start, n)
+        both = _chunked(lambda a, c: np.vstack(adversarial_config(c, 4, a)), start, n, workers, axis=1)
+        return ("soa", np.ascontiguousarray(both[:24]), np.ascontiguousarray(both[24]))
+    verts, idx = indexed_config(cfg, start, n, slab=slab, workers=workers)
     return ("indexed", verts, idx)

@@ -239,6 +239,17 @@ hexval_profile* hexval_profile_create(void);
 void hexval_profile_destroy(hexval_profile* p);
 int hexval_profile_read(hexval_profile* p, double* ms_out, long long* launches_out);
 
+/* ---- roofline probe (diag.cu; not the hot path) --------------------------
+ * Measured FP64 pipe throughput of the current device, the denominator of the
+ * FP64 rooflines (the subdivision kernel and indexed pass 1 are
+ * FP64 bound): a DFMA-only kernel (8 independent chains per thread, 8 x 256
+ * threads per SM, `iters` iterations, best of 5 timed launches on `stream`).
+ * *dfma_per_s_out = DFMA lane-instructions per second (1 DFMA = 2 flops);
+ * *best_ms_out (optional) = the best launch time.  Synchronises `stream`.
+ * Returns HEXVAL_OK, HEXVAL_ERR_ARGUMENT (iters <= 0 or NULL output),
+ * HEXVAL_ERR_ALLOC or HEXVAL_ERR_CUDA.                                      */
+int hexval_diag_fp64_peak(int iters, double* dfma_per_s_out, float* best_ms_out, cudaStream_t stream);
+
 /* ---- misc -------------------------------------------------------------- */
 const char* hexval_status_string(int status);
 int hexval_version(void);              /* 100 * major + minor                */

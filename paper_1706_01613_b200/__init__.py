@@ -25,6 +25,7 @@ __all__ = [
     "check_indexed_host", "classify_bezier", "Stats", "Profile", "status_string", "version",
     "kernel_launches_per_call", "corner_quality_soa", "corner_quality_indexed", "min_detj_bounds_soa",
     "min_detj_bounds_indexed", "select_valid", "check_quad_soa", "check_screen_soa", "check_screen_indexed",
+    "fp64_peak",
 ]
 
 INVALID, VALID, UNDETERMINED, NONFINITE = 0, 1, 2, 3
@@ -82,6 +83,8 @@ def _load() -> ctypes.CDLL:
     L.hexval_select_valid.restype = ctypes.c_int
     L.hexval_check_quad_soa.argtypes = [_vp, _i64, _vp, _vp, _vp]
     L.hexval_check_quad_soa.restype = ctypes.c_int
+    L.hexval_diag_fp64_peak.argtypes = [ctypes.c_int, _vp, _vp, _vp]
+    L.hexval_diag_fp64_peak.restype = ctypes.c_int
     L.hexval_status_string.argtypes = [ctypes.c_int]
     L.hexval_status_string.restype = ctypes.c_char_p
     L.hexval_profile_create.argtypes = []
@@ -113,6 +116,16 @@ def version() -> int:
 
 def kernel_launches_per_call() -> int:
     return lib().hexval_kernel_launches_per_call()
+
+
+def fp64_peak(iters: int = 4096, stream=None) -> dict:
+    """hexval_diag_fp64_peak: measured DFMA lane-instructions/s of the current device (roofline
+    denominator of the FP64-bound kernels).  Synchronises the stream."""
+    rate = ctypes.c_double()
+    ms = ctypes.c_float()
+    _check(lib().hexval_diag_fp64_peak(int(iters), ctypes.byref(rate), ctypes.byref(ms), _stream_handle(stream)),
+           "hexval_diag_fp64_peak")
+    return {"dfma_per_s": rate.value, "best_ms": ms.value}
 
 
 def _check(code: int, what: str) -> None:

@@ -8,7 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "hexval.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "hexval_device.cuh"), os.path.join(ROOT, "include", "hexval.h")]
+SRC_DIAG = os.path.join(HERE, "csrc", "diag.cu")      # roofline probes (not the hot path)
+DEPS = [SRC, SRC_DIAG, os.path.join(HERE, "csrc", "hexval_device.cuh"), os.path.join(ROOT, "include", "hexval.h")]
 LIB = os.path.join(HERE, "libhexval.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -35,7 +36,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     target = out or LIB
     if out is None and not force and not needs_build():
         return LIB
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", target, SRC]
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", target, SRC, SRC_DIAG]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as fh:
