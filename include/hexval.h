@@ -92,7 +92,10 @@ typedef struct hexval_profile hexval_profile;
  * stream       CUDA stream; all work is enqueued on it, results are valid
  *              after the stream synchronises.  No host synchronisation
  *              happens inside the call.  Calls on different streams are
- *              independent (scratch is stream-ordered cudaMallocAsync).
+ *              independent: scratch (control block, work queues, the
+ *              subdivision stacks) is borrowed from persistent library-owned
+ *              arenas, one per stream with calls in flight, stream-ordered
+ *              (see hexval_scratch_info); steady-state calls allocate nothing.
  * Device       the calling thread's current device (cudaSetDevice): every
  *              device buffer and the stream must belong to it.
  * Ownership    the caller owns every buffer; the library never frees them.
@@ -238,6 +241,24 @@ int hexval_check_indexed_host(const double* vertices_host, int64_t nv,
 hexval_profile* hexval_profile_create(void);
 void hexval_profile_destroy(hexval_profile* p);
 int hexval_profile_read(hexval_profile* p, double* ms_out, long long* launches_out);
+
+/* ---- scratch ----------------------------------------------------------------
+ * The library owns a memory pool per device (cudaMemPoolCreate; the process's
+ * default pool is not modified) and persistent scratch arenas carved from it:
+ * a call borrows the arena its stream used last, else an arena whose last use
+ * has completed, else a new one (arenas = streams with calls in flight at the
+ * same time).  An arena holds a 256-B control block, two int32 queues of n
+ * entries and the subdivision kernel's node stacks (~1.1 MB per resident warp,
+ * the depth-sorted stack's worst case); it grows only when a call needs more.
+ * Calls enqueued during CUDA-graph capture allocate from the pool per call
+ * instead (graph memory nodes).
+ * hexval_scratch_info: bytes reserved by the arenas of `device` and their
+ *   number (either output may be NULL).  Host-only; no CUDA call.
+ * hexval_scratch_release: frees every idle arena of the current device (waits
+ *   for their last uses) and trims the pool.  Returns HEXVAL_OK or
+ *   HEXVAL_ERR_CUDA.                                                          */
+int hexval_scratch_info(int device, size_t* bytes_reserved_out, int* arenas_out);
+int hexval_scratch_release(void);
 
 /* ---- roofline probe (diag.cu; not the hot path) --------------------------
  * Measured FP64 pipe throughput of the current device, the denominator of the

@@ -25,7 +25,7 @@ __all__ = [
     "check_indexed_host", "classify_bezier", "Stats", "Profile", "status_string", "version",
     "kernel_launches_per_call", "corner_quality_soa", "corner_quality_indexed", "min_detj_bounds_soa",
     "min_detj_bounds_indexed", "select_valid", "check_quad_soa", "check_screen_soa", "check_screen_indexed",
-    "fp64_peak",
+    "fp64_peak", "scratch_info", "scratch_release",
 ]
 
 INVALID, VALID, UNDETERMINED, NONFINITE = 0, 1, 2, 3
@@ -83,6 +83,10 @@ def _load() -> ctypes.CDLL:
     L.hexval_select_valid.restype = ctypes.c_int
     L.hexval_check_quad_soa.argtypes = [_vp, _i64, _vp, _vp, _vp]
     L.hexval_check_quad_soa.restype = ctypes.c_int
+    L.hexval_scratch_info.argtypes = [ctypes.c_int, _vp, _vp]
+    L.hexval_scratch_info.restype = ctypes.c_int
+    L.hexval_scratch_release.argtypes = []
+    L.hexval_scratch_release.restype = ctypes.c_int
     L.hexval_diag_fp64_peak.argtypes = [ctypes.c_int, _vp, _vp, _vp]
     L.hexval_diag_fp64_peak.restype = ctypes.c_int
     L.hexval_status_string.argtypes = [ctypes.c_int]
@@ -116,6 +120,21 @@ def version() -> int:
 
 def kernel_launches_per_call() -> int:
     return lib().hexval_kernel_launches_per_call()
+
+
+def scratch_info(device: int | None = None) -> dict:
+    """hexval_scratch_info: bytes reserved by the library's scratch arenas on `device` and their number."""
+    if device is None:
+        device = _torch().cuda.current_device()
+    b = ctypes.c_size_t()
+    c = ctypes.c_int()
+    _check(lib().hexval_scratch_info(int(device), ctypes.byref(b), ctypes.byref(c)), "hexval_scratch_info")
+    return {"bytes": b.value, "arenas": c.value}
+
+
+def scratch_release() -> None:
+    """hexval_scratch_release: free the idle scratch arenas of the current device."""
+    _check(lib().hexval_scratch_release(), "hexval_scratch_release")
 
 
 def fp64_peak(iters: int = 4096, stream=None) -> dict:

@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "hexval.cu")
 SRC_DIAG = os.path.join(HERE, "csrc", "diag.cu")      # roofline probes (not the hot path)
-DEPS = [SRC, SRC_DIAG, os.path.join(HERE, "csrc", "hexval_device.cuh"), os.path.join(ROOT, "include", "hexval.h")]
+DEPS = [SRC, SRC_DIAG, os.path.join(HERE, "csrc", "hexval_device.cuh"), os.path.join(HERE, "csrc", "scratch.cuh"),
+        os.path.join(ROOT, "include", "hexval.h")]
 LIB = os.path.join(HERE, "libhexval.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

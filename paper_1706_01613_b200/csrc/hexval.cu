@@ -33,6 +33,7 @@
 
 #include "hexval.h"
 #include "hexval_device.cuh"
+#include "scratch.cuh"
 
 using namespace hexval;
 
@@ -957,6 +958,7 @@ __device__ __forceinline__ void split_quarter_s(const double* G1, int hx, int hy
     }
 }
 
+
 struct K4Warp {
     unsigned status[32];    // per batch slot: bit 0 INVALID found, bit 1 depth cap reached
     uint32_t hex[32];       // hex id of each batch slot
@@ -1735,12 +1737,6 @@ const DeviceInfo& device_info(int dev) {
         const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup() : 0);
         d.p1_variant = ctas > 0 ? want : P1_LDG;
         d.p1_ctas_per_sm = ctas > 0 ? ctas : 1;
-        // keep freed stream-ordered scratch in the pool between calls
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
         d.ok = true;
     }
     return d;
@@ -1888,11 +1884,12 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
     const size_t total = ctl_bytes + 2 * q_bytes + sc_bytes;
-    char* base = nullptr;
-    if (cudaMallocAsync((void**)&base, total, stream) != cudaSuccess) {
+    hexval_scratch::Lease lease;
+    if (hexval_scratch::acquire(lease, total, stream) != cudaSuccess) {
         cudaGetLastError();
         return HEXVAL_ERR_ALLOC;
     }
+    char* const base = lease.base;
     Ctl* ctl = reinterpret_cast<Ctl*>(base);
     uint32_t* qsub = reinterpret_cast<uint32_t*>(base + ctl_bytes);
     uint32_t* qex = reinterpret_cast<uint32_t*>(base + ctl_bytes + q_bytes);
@@ -1913,7 +1910,7 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     const CoordRoot<L> root{ld};
     launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, qex, fr, stats, stream);
     mark(HEXVAL_PHASE_SUBDIV, 1);
-    cudaFreeAsync(base, stream);
+    hexval_scratch::release(lease, stream);
     if (cudaGetLastError() != cudaSuccess) return HEXVAL_ERR_CUDA;
     return HEXVAL_OK;
 }
@@ -1960,11 +1957,12 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
-    char* base = nullptr;
-    if (cudaMallocAsync((void**)&base, ctl_bytes + q_bytes + sc_bytes, stream) != cudaSuccess) {
+    hexval_scratch::Lease lease;
+    if (hexval_scratch::acquire(lease, ctl_bytes + q_bytes + sc_bytes, stream) != cudaSuccess) {
         cudaGetLastError();
         return HEXVAL_ERR_ALLOC;
     }
+    char* const base = lease.base;
     Ctl* ctl = reinterpret_cast<Ctl*>(base);
     uint32_t* qsub = reinterpret_cast<uint32_t*>(base + ctl_bytes);
     WarpStacks fr;
@@ -1975,7 +1973,7 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     else bezier_pass_kernel<false><<<p1_blocks, P1_THREADS, 0, stream>>>(b, n, flags, ctl, qsub, stats);
     const CoeffRoot root{b, n};
     launch_subdiv(root, info, k4_blocks, flags, ctl, qsub, qsub, fr, stats, stream);
-    cudaFreeAsync(base, stream);
+    hexval_scratch::release(lease, stream);
     if (cudaGetLastError() != cudaSuccess) return HEXVAL_ERR_CUDA;
     return HEXVAL_OK;
 }
@@ -2001,11 +1999,12 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     const size_t warps = (size_t)blocks * K4_WARPS;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
     const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
-    char* base = nullptr;
-    if (cudaMallocAsync((void**)&base, 256 + q_bytes + sc_bytes, stream) != cudaSuccess) {
+    hexval_scratch::Lease lease;
+    if (hexval_scratch::acquire(lease, 256 + q_bytes + sc_bytes, stream) != cudaSuccess) {
         cudaGetLastError();
         return HEXVAL_ERR_ALLOC;
     }
+    char* const base = lease.base;
     unsigned* ctlq = reinterpret_cast<unsigned*>(base);          // [0] queue length, [1] fetch cursor
     uint32_t* q = reinterpret_cast<uint32_t*>(base + 256);
     WarpStacks ws;
@@ -2014,7 +2013,7 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     launch_bounds_root(ld, n, BoundsRootBody{rel_tol, lower, upper, status, ctlq, q}, stream);
     bounds_kernel<L><<<(unsigned)blocks, K4_THREADS, 0, stream>>>(ld, rel_tol, lower, upper, status, ctlq, q, ws,
                                                                     nodes_dev_opt);
-    cudaFreeAsync(base, stream);
+    hexval_scratch::release(lease, stream);
     return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
 }
 
@@ -2129,15 +2128,16 @@ int hexval_select_valid(const uint8_t* flags, int64_t n, const int32_t* group_op
     if (misaligned(ids_out_opt, 4) || misaligned(group_opt, 4) || misaligned(group_counts_opt, 4))
         return HEXVAL_ERR_ALIGNMENT;
     const int64_t tiles = (n + SEL_TILE - 1) / SEL_TILE;
-    unsigned* tc = nullptr;
-    if (cudaMallocAsync((void**)&tc, (size_t)tiles * sizeof(unsigned), stream) != cudaSuccess) {
+    hexval_scratch::Lease lease;
+    if (hexval_scratch::acquire(lease, (size_t)tiles * sizeof(unsigned), stream) != cudaSuccess) {
         cudaGetLastError();
         return HEXVAL_ERR_ALLOC;
     }
+    unsigned* tc = reinterpret_cast<unsigned*>(lease.base);
     select_count_kernel<<<(unsigned)tiles, SEL_THREADS, 0, stream>>>(flags, n, group_opt, group_counts_opt, tc);
     select_scan_kernel<<<1, 1024, 0, stream>>>(tc, tiles, count_dev);
     if (ids_out_opt) select_write_kernel<<<(unsigned)tiles, SEL_THREADS, 0, stream>>>(flags, n, tc, ids_out_opt);
-    cudaFreeAsync(tc, stream);
+    hexval_scratch::release(lease, stream);
     return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
 }
 
@@ -2201,9 +2201,9 @@ int hexval_check_soa_host(const double* coords_host, int64_t n, uint8_t* flags_h
     uint8_t* df[2] = {nullptr, nullptr};
     double* dk[2] = {nullptr, nullptr};
     for (int k = 0; k < 2 && rc == HEXVAL_OK; ++k) {
-        if (cudaMallocAsync((void**)&dc[k], (size_t)24 * C * sizeof(double), hp.s[k]) != cudaSuccess ||
-            cudaMallocAsync((void**)&df[k], (size_t)C, hp.s[k]) != cudaSuccess ||
-            (coeffs_host_opt && cudaMallocAsync((void**)&dk[k], (size_t)27 * C * sizeof(double), hp.s[k]) != cudaSuccess))
+        if (hexval_scratch::alloc_async((void**)&dc[k], (size_t)24 * C * sizeof(double), hp.s[k]) != cudaSuccess ||
+            hexval_scratch::alloc_async((void**)&df[k], (size_t)C, hp.s[k]) != cudaSuccess ||
+            (coeffs_host_opt && hexval_scratch::alloc_async((void**)&dk[k], (size_t)27 * C * sizeof(double), hp.s[k]) != cudaSuccess))
             rc = HEXVAL_ERR_ALLOC;
     }
     for (int64_t off = 0, it = 0; off < n && rc == HEXVAL_OK; off += C, ++it) {
@@ -2245,7 +2245,7 @@ int hexval_check_indexed_host(const double* vertices_host, int64_t nv, const int
     double* dk[2] = {nullptr, nullptr};
     cudaEvent_t vready = nullptr;
     if (rc == HEXVAL_OK) {
-        if (cudaMallocAsync((void**)&dv, (size_t)3 * nv * sizeof(double) + 8, hp.s[0]) != cudaSuccess) rc = HEXVAL_ERR_ALLOC;
+        if (hexval_scratch::alloc_async((void**)&dv, (size_t)3 * nv * sizeof(double) + 8, hp.s[0]) != cudaSuccess) rc = HEXVAL_ERR_ALLOC;
         else {
             cudaMemcpyAsync(dv, vertices_host, (size_t)3 * nv * sizeof(double), cudaMemcpyHostToDevice, hp.s[0]);
             cudaEventCreateWithFlags(&vready, cudaEventDisableTiming);
@@ -2254,9 +2254,9 @@ int hexval_check_indexed_host(const double* vertices_host, int64_t nv, const int
         }
     }
     for (int k = 0; k < 2 && rc == HEXVAL_OK; ++k) {
-        if (cudaMallocAsync((void**)&di[k], (size_t)8 * C * sizeof(int32_t), hp.s[k]) != cudaSuccess ||
-            cudaMallocAsync((void**)&df[k], (size_t)C, hp.s[k]) != cudaSuccess ||
-            (coeffs_host_opt && cudaMallocAsync((void**)&dk[k], (size_t)27 * C * sizeof(double), hp.s[k]) != cudaSuccess))
+        if (hexval_scratch::alloc_async((void**)&di[k], (size_t)8 * C * sizeof(int32_t), hp.s[k]) != cudaSuccess ||
+            hexval_scratch::alloc_async((void**)&df[k], (size_t)C, hp.s[k]) != cudaSuccess ||
+            (coeffs_host_opt && hexval_scratch::alloc_async((void**)&dk[k], (size_t)27 * C * sizeof(double), hp.s[k]) != cudaSuccess))
             rc = HEXVAL_ERR_ALLOC;
     }
     for (int64_t off = 0, it = 0; off < n && rc == HEXVAL_OK; off += C, ++it) {
@@ -2333,7 +2333,20 @@ const char* hexval_status_string(int status) {
     }
 }
 
-int hexval_version(void) { return 120; }
+int hexval_scratch_info(int device, size_t* bytes_reserved_out, int* arenas_out) {
+    if (device < 0 || device >= 64) return HEXVAL_ERR_ARGUMENT;
+    hexval_scratch::info(device, bytes_reserved_out, arenas_out);
+    return HEXVAL_OK;
+}
+
+int hexval_scratch_release(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return HEXVAL_ERR_CUDA;
+    hexval_scratch::release_all(dev);
+    return cudaGetLastError() == cudaSuccess ? HEXVAL_OK : HEXVAL_ERR_CUDA;
+}
+
+int hexval_version(void) { return 200; }
 
 int hexval_kernel_launches_per_call(void) { return 2; }
 

@@ -221,6 +221,37 @@ def test_side_stream_matches_default_stream():
     assert np.array_equal(f1.cpu().numpy(), f0) and np.array_equal(f2.cpu().numpy(), f0)
 
 
+def test_scratch_arenas_are_persistent_and_per_stream():
+    """Scratch is borrowed from persistent library-owned arenas: a repeated call
+    on the same stream allocates nothing (the reserved bytes do not change), a second stream
+    with work in flight gets its own arena, and hexval_scratch_release frees them."""
+    hv.scratch_release()
+    assert hv.scratch_info()["arenas"] == 0
+    coords = torch.from_numpy(hexgen.soa_config(2_000_000, 0.35, 1)).cuda()
+    f0, _ = hv.check_soa(coords)
+    torch.cuda.synchronize()
+    a = hv.scratch_info()
+    assert a["arenas"] == 1 and a["bytes"] > 0
+    for _ in range(3):
+        f1, _ = hv.check_soa(coords)
+    torch.cuda.synchronize()
+    assert hv.scratch_info() == a                               # steady state: no allocation
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out = []
+    for st in (s1, s2):
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            out.append(hv.check_soa(coords)[0])
+    torch.cuda.synchronize()
+    assert all(torch.equal(o, f0) for o in out) and torch.equal(f1, f0)
+    assert 1 <= hv.scratch_info()["arenas"] <= 3
+    hv.scratch_release()
+    assert hv.scratch_info() == {"bytes": 0, "arenas": 0}
+    f2, _ = hv.check_soa(coords)                                # works again after a release
+    torch.cuda.synchronize()
+    assert torch.equal(f2, f0)
+
+
 def test_concurrent_calls_on_two_streams_and_threads():
     """Scratch is per call and device setup is guarded, so calls from two host
     threads on two streams (ctypes releases the GIL) give the single-call results."""
