@@ -111,6 +111,7 @@ struct IdxLoader {
     static constexpr bool kIntStep2 = true;      // see step2_class
     const double* __restrict__ verts;
     const int32_t* __restrict__ idx;
+    const uint8_t* dupf = nullptr;               // optional: precomputed duplicate-id flag of this thread's hex (smem)
     __device__ __forceinline__ void load(int64_t i, double* X) const {
         int v[8];
         if ((((uintptr_t)idx) & 15) == 0) {
@@ -136,10 +137,7 @@ struct IdxLoader {
 
 // NONFINITE (reading G13): a coordinate is NaN/Inf or |x| > 2^300
 __device__ __forceinline__ bool out_of_range(const double* X) {
-    int mk = 0;
-#pragma unroll
-    for (int p = 0; p < 24; ++p) mk = max(mk, abskey(X[p]));
-    if (mk < 0x52B00000) return false;                 // every |x| < 2^300
+    if (max_abskey<24>(X) < 0x52B00000) return false;   // every |x| < 2^300
     bool bad = false;
 #pragma unroll
     for (int p = 0; p < 24; ++p) bad |= !(fabs(X[p]) <= 0x1p300);
@@ -167,7 +165,15 @@ __device__ __forceinline__ bool face_pair_coincident(const double* X) {
     return hit;
 }
 
+__device__ __forceinline__ bool ids_dup_face_pair(const int* v) {
+    bool hit = false;
+#pragma unroll
+    for (int q = 0; q < 24; ++q) hit |= v[kFacePairs[q][0]] == v[kFacePairs[q][1]];
+    return hit;
+}
+
 __device__ __forceinline__ bool IdxLoader::dup_face_pair(int64_t i) const {
+    if (dupf) return *dupf != 0;
     int v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = __ldg(idx + 8 * i + k);
@@ -598,16 +604,24 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
     soa_cp_kernel(const double* __restrict__ coords, int64_t n, Body body) {
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS]
     const int tid = threadIdx.x;
-    const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
+    // 32-bit tile counters (n <= INT32_MAX): loop state that fits one register each, so the
+    // register allocator does not spill it next to the hex's values
+#ifdef HEXVAL_LOOP64
+    using tile_t = int64_t;                                  // A/B build: round 1's 64-bit loop state
+#else
+    using tile_t = int;
+#endif
+    const tile_t tiles = (tile_t)((n + CP_THREADS - 1) / CP_THREADS);
+    const tile_t G = (tile_t)gridDim.x;
     const uint32_t s0 = smem_u32(cp_buf + tid);
     const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
-    int64_t t = blockIdx.x;
-    cp_issue_hex(coords, n, t * CP_THREADS + tid, s0);
-    cp_issue_hex(coords, n, (t + gridDim.x) * CP_THREADS + tid, s1);
-    for (int k = 0; t < tiles; t += gridDim.x, ++k) {
+    tile_t t = blockIdx.x;
+    cp_issue_hex(coords, n, (int64_t)t * CP_THREADS + tid, s0);
+    cp_issue_hex(coords, n, (int64_t)(t + G) * CP_THREADS + tid, s1);
+    for (int k = 0; t < tiles; t += G, ++k) {
         const int b = k & 1;
         cp_async_wait1();                                    // tile k has landed (tile k+1 may be in flight)
-        const int64_t i = t * CP_THREADS + tid;
+        const int64_t i = (int64_t)t * CP_THREADS + tid;
         int st = -1;
         if (i < n) {
             const double* src = cp_buf + b * 24 * CP_THREADS + tid;
@@ -617,7 +631,7 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
             st = body.hex(SoaLoader{coords, n}, X, i);
         }
         // refill this buffer with tile k+2 (X was consumed above: program order)
-        cp_issue_hex(coords, n, (t + 2 * (int64_t)gridDim.x) * CP_THREADS + tid, b ? s1 : s0);
+        cp_issue_hex(coords, n, (int64_t)(t + 2 * G) * CP_THREADS + tid, b ? s1 : s0);
         body.epilogue(st, i);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -631,7 +645,7 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
 // connectivity row of tile k+2 (two 16-byte async copies into shared memory);
 // after computing, the thread reads that row from shared memory and issues the
 // gathers of tile k+2.  No register holds prefetched data across the compute.
-constexpr size_t CPI_SMEM = CP_SMEM + (size_t)2 * CP_THREADS * 32;   // + two idx tiles
+constexpr size_t CPI_SMEM = CP_SMEM + (size_t)2 * CP_THREADS * 32 + (size_t)2 * CP_THREADS;   // + two idx tiles, two dup-flag tiles
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
@@ -645,11 +659,16 @@ __device__ __forceinline__ void cp_idx_row(const int32_t* __restrict__ idx, int6
 }
 
 __device__ __forceinline__ void cp_gather_row(const double* __restrict__ verts, int64_t n, int64_t i,
-                                              const int32_t* row, uint32_t dst) {
+                                              const int32_t* row, uint32_t dst, uint8_t* dupf) {
     if (i < n) {
         const int4 a = *reinterpret_cast<const int4*>(row);
         const int4 b = *reinterpret_cast<const int4*>(row + 4);
         const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        // the coincident-node rule on the ids while they are at hand: read back only by
+        // hexes whose Step 2 is not decided in fp64 (IdxLoader::dup_face_pair)
+#ifndef HEXVAL_NO_DUPFLAG
+        *dupf = ids_dup_face_pair(v);
+#endif
         uint64_t policy;
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(policy));
 #pragma unroll
@@ -666,41 +685,48 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
     idx_cp_kernel(const double* __restrict__ verts, const int32_t* __restrict__ idx, int64_t n, Body body) {
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS] coords, then [2][CP_THREADS][8] ids
     const int tid = threadIdx.x;
-    const int64_t tiles = (n + CP_THREADS - 1) / CP_THREADS;
-    const int64_t G = gridDim.x;
+    const int tiles = (int)((n + CP_THREADS - 1) / CP_THREADS);   // 32-bit loop state (see soa_cp_kernel)
+    const int G = (int)gridDim.x;
     const uint32_t s0 = smem_u32(cp_buf + tid);
     const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
     int32_t* const rows = reinterpret_cast<int32_t*>(cp_buf + 2 * 24 * CP_THREADS);
     int32_t* const row0 = rows + 8 * tid;                     // id row of tiles with even k
     int32_t* const row1 = rows + 8 * (CP_THREADS + tid);      // ... odd k
+    uint8_t* const dupf = reinterpret_cast<uint8_t*>(rows + 16 * CP_THREADS);
+    uint8_t* const dup0 = dupf + tid;                         // duplicate-id flag of tiles with even k
+    uint8_t* const dup1 = dupf + CP_THREADS + tid;            // ... odd k
     const uint32_t r0 = smem_u32(row0), r1 = smem_u32(row1);
-    const IdxLoader ld{verts, idx};
-    int64_t t = blockIdx.x;
+    int t = blockIdx.x;
+    auto hex_of = [&](int tile) { return (int64_t)tile * CP_THREADS + tid; };
     // prologue: rows of tiles 0 and 1 synchronously, then groups G0 = {gathers 0, row 2}, G1 = {gathers 1, row 3}
-    cp_idx_row(idx, n, t * CP_THREADS + tid, r0);
-    cp_idx_row(idx, n, (t + G) * CP_THREADS + tid, r1);
+    cp_idx_row(idx, n, hex_of(t), r0);
+    cp_idx_row(idx, n, hex_of(t + G), r1);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    cp_gather_row(verts, n, t * CP_THREADS + tid, row0, s0);
-    cp_idx_row(idx, n, (t + 2 * G) * CP_THREADS + tid, r0);
+    cp_gather_row(verts, n, hex_of(t), row0, s0, dup0);
+    cp_idx_row(idx, n, hex_of(t + 2 * G), r0);
     cp_async_commit();
-    cp_gather_row(verts, n, (t + G) * CP_THREADS + tid, row1, s1);
-    cp_idx_row(idx, n, (t + 3 * G) * CP_THREADS + tid, r1);
+    cp_gather_row(verts, n, hex_of(t + G), row1, s1, dup1);
+    cp_idx_row(idx, n, hex_of(t + 3 * G), r1);
     cp_async_commit();
     for (int k = 0; t < tiles; t += G, ++k) {
         const int bb = k & 1;
         cp_async_wait1();                                    // group k: coords of tile k, row of tile k+2
-        const int64_t i = t * CP_THREADS + tid;
+        const int64_t i = hex_of(t);
         int st = -1;
         if (i < n) {
             const double* src = cp_buf + bb * 24 * CP_THREADS + tid;
             double X[24];
 #pragma unroll
             for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
-            st = body.hex(ld, X, i);
+#ifndef HEXVAL_NO_DUPFLAG
+            st = body.hex(IdxLoader{verts, idx, bb ? dup1 : dup0}, X, i);
+#else
+            st = body.hex(IdxLoader{verts, idx}, X, i);
+#endif
         }
         // group k+2: gathers of tile k+2 (row read from shared memory), row of tile k+4
-        cp_gather_row(verts, n, (t + 2 * G) * CP_THREADS + tid, bb ? row1 : row0, bb ? s1 : s0);
-        cp_idx_row(idx, n, (t + 4 * G) * CP_THREADS + tid, bb ? r1 : r0);
+        cp_gather_row(verts, n, hex_of(t + 2 * G), bb ? row1 : row0, bb ? s1 : s0, bb ? dup1 : dup0);
+        cp_idx_row(idx, n, hex_of(t + 4 * G), bb ? r1 : r0);
         cp_async_commit();
         body.epilogue(st, i);
     }

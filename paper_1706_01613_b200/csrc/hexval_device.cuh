@@ -44,6 +44,42 @@ __device__ __forceinline__ double det3(const V3& a, const V3& b, const V3& c) {
 __device__ __forceinline__ int key(double x) { return __double2hiint(x); }
 __device__ __forceinline__ int abskey(double x) { return __double2hiint(x) & 0x7fffffff; }
 
+// max of abskey over N values: masked keys, a serial chain of maxima (the
+// compiler forms 3-input VIMNMX3); measured equal to a balanced tree and 2-10%
+// faster than signed/unsigned maxima of the raw keys, which need no masks but
+// two reductions (profiles/r02/PASS1_EXPERIMENTS.md).
+template <int N>
+__device__ __forceinline__ int max3_tree(const int* k) {
+    if constexpr (N == 1) return k[0];
+    else if constexpr (N == 2) return max(k[0], k[1]);
+    else {
+        constexpr int M = (N + 2) / 3;
+        int r[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const int a = k[3 * j];
+            const int b = 3 * j + 1 < N ? k[3 * j + 1] : a;
+            const int c = 3 * j + 2 < N ? k[3 * j + 2] : a;
+            r[j] = max(a, max(b, c));
+        }
+        return max3_tree<M>(r);
+    }
+}
+template <int N>
+__device__ __forceinline__ int max_abskey(const double* x) {
+#ifndef HEXVAL_ABSKEY_TREE
+    int m = 0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) m = max(m, abskey(x[j]));
+    return m;
+#else
+    int a[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) a[j] = abskey(x[j]);
+    return max3_tree<N>(a);
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // S1 + S2: the 20 Jacobian samples as tetrahedron determinants (section 5,
 // PAPER.md:819-878, Fig. 4).  X[3k + a] = axis a of node k (Fig. 3 order).
@@ -75,12 +111,10 @@ __device__ __forceinline__ void samples20(const double* X, Samples& s, CornerHoo
     const V3 v12 = vsub(n2, n1), v43 = vsub(n3, n4), v56 = vsub(n6, n5), v87 = vsub(n7, n8);
     const V3 v14 = vsub(n4, n1), v23 = vsub(n3, n2), v58 = vsub(n8, n5), v67 = vsub(n7, n6);
     const V3 v15 = vsub(n5, n1), v26 = vsub(n6, n2), v48 = vsub(n8, n4), v37 = vsub(n7, n3);
-    int e = 0;
-#define HV_EK(v) e = max(e, max(abskey(v.x), max(abskey(v.y), abskey(v.z))))
-    HV_EK(v12); HV_EK(v43); HV_EK(v56); HV_EK(v87);
-    HV_EK(v14); HV_EK(v23); HV_EK(v58); HV_EK(v67);
-    HV_EK(v15); HV_EK(v26); HV_EK(v48); HV_EK(v37);
-#undef HV_EK
+    const double comps[36] = {v12.x, v12.y, v12.z, v43.x, v43.y, v43.z, v56.x, v56.y, v56.z, v87.x, v87.y, v87.z,
+                              v14.x, v14.y, v14.z, v23.x, v23.y, v23.z, v58.x, v58.y, v58.z, v67.x, v67.y, v67.z,
+                              v15.x, v15.y, v15.z, v26.x, v26.y, v26.z, v48.x, v48.y, v48.z, v37.x, v37.y, v37.z};
+    const int e = max_abskey<36>(comps);
     s.ekey = e;
 
     // corners: det(d_xi x, d_eta x, d_zeta x) with the 3 edges at the corner
