@@ -27,6 +27,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
@@ -82,6 +84,9 @@ def parse():
                    help="also time the call captured in a CUDA graph (launch-bound small batches)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
+    p.add_argument("--ref-seconds", type=float, default=150.0,
+                   help="reference arm: wall-time budget of all warm-up + timed steps (whole configuration per "
+                        "step when it fits, else a prefix sample)")
     p.add_argument("--coeffs", action="store_true",
                    help="also write the 27 Bezier coefficients per hex (409 B/hex, SURVEY.md 8(d))")
     p.add_argument("--op", choices=["check", "quality", "screen", "bounds", "select", "quads"], default="check",
@@ -294,27 +299,47 @@ def oracle_rate(cfg: int, seconds: float, start: int = 0, gpu_flags=None, worker
 
 
 def run_reference(args, world, rank):
-    import hexgen
+    """The reference arm: the CPU oracle, as it stands, on the host cores, timed per step on the
+    whole configuration when the K steps fit the time budget (--ref-seconds), else on a prefix
+    sample of the configuration sized to it."""
+    import oracle
     if rank != 0:
         return 0
-    n = hexgen.config_size(args.config)
-    per_step = []
+    layout, n, host = make_inputs(args.config, 0, args.workers)
+    cores = oracle.num_threads(0)
+
+    def run(m):
+        if layout == "soa":
+            return oracle.check_soa(np.ascontiguousarray(host[0][:, :m]))
+        return oracle.check_indexed(host[0], np.ascontiguousarray(host[1][:m]))
+
+    probe = min(n, 20_000)
+    run(probe)                                                # warm: thread pool, page-in
+    t0 = time.perf_counter()
+    run(probe)
+    est = (time.perf_counter() - t0) * n / probe             # seconds for the whole configuration
+    budget = args.ref_seconds / max(1, args.steps + args.warmup)
+    m = n if est <= budget else max(probe, int(n * budget / est))
     for _ in range(args.warmup):
-        oracle_rate(args.config, min(args.cpu_seconds, 2.0))
-    last = None
+        run(min(m, probe * 4))
+    per_step = []
     for _ in range(args.steps):
-        last = oracle_rate(args.config, args.cpu_seconds / max(1, args.steps) + 0.5)
-        per_step.append(last["value"])
+        t0 = time.perf_counter()
+        run(m)
+        per_step.append(m / (time.perf_counter() - t0))
     value = statistics.median(per_step)
+    whole = m == n
+    sample = (f"hexes 0..{m - 1} of {CONFIG_DESC[args.config]} ({m} hexes per step"
+              f"{', the whole configuration' if whole else ', a prefix sample'}, {cores} threads)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_DESC[args.config], "n_hexes": n,
-                   "layout": "indexed" if args.config in (2, 3) else "soa",
-                   "note": "each step times the CPU oracle (oracle/, as it stands) on a bounded prefix sample; ms_per_step is extrapolated to the full batch"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
-                         "sample": last["sample"]},
+        "config": {"workload": CONFIG_DESC[args.config], "n_hexes": n, "layout": layout,
+                   "note": ("each step runs the CPU oracle (oracle/, as it stands) on the whole configuration"
+                            if whole else "each step times the CPU oracle (oracle/, as it stands) on a bounded "
+                            "prefix sample; ms_per_step is extrapolated to the full batch")},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
