@@ -343,14 +343,14 @@ __device__ __forceinline__ void corner_quality(const V3* E, const double* c, int
                          __dmul_rn(__dmul_rn(l56, l58), l15), __dmul_rn(__dmul_rn(l56, l67), l26),
                          __dmul_rn(__dmul_rn(l87, l67), l37), __dmul_rn(__dmul_rn(l87, l58), l48)};
     int km = key(c[0]);
-    double bn = __dmul_rn(c[0], fabs(c[0])), bp = P[0];
+    double bn = __dmul_rn(c[0], fabs(c[0])), bp = P[0], bc = c[0];
     bool zero_edge = !(P[0] > 0.0);
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
         km = min(km, key(c[k]));
         zero_edge |= !(P[k] > 0.0);
         const double nk = __dmul_rn(c[k], fabs(c[k]));
-        if (__dmul_rn(nk, bp) < __dmul_rn(bn, P[k])) { bn = nk; bp = P[k]; }   // nk/P[k] < bn/bp
+        if (__dmul_rn(nk, bp) < __dmul_rn(bn, P[k])) { bn = nk; bp = P[k]; bc = c[k]; }   // nk/P[k] < bn/bp
     }
     const int T = key(step2_tau(ekey));                // tau2 > 0: key == abskey
     if (km > T) {
@@ -361,7 +361,8 @@ __device__ __forceinline__ void corner_quality(const V3* E, const double* c, int
         for (int k = 1; k < 8; ++k) um = max(um, (unsigned)key(c[k]));
         t1 = um > (0x80000000u | (unsigned)T) ? 0 : T1_PENDING;   // a robustly negative corner, else exact
     }
-    sj = zero_edge ? __longlong_as_double(0x7ff8000000000000ll) : copysign(sqrt(__ddiv_rn(fabs(bn), bp)), bn);
+    // the winner's c / sqrt(P) as c * rsqrt(P) (a few ulps; the parity tolerance is 1e-13)
+    sj = zero_edge ? __longlong_as_double(0x7ff8000000000000ll) : __dmul_rn(bc, rsqrt(bp));
 }
 
 // S1-S5 + S8 for one hex whose 24 coordinates are in registers; returns the

@@ -969,6 +969,23 @@ def test_power_of_two_scaling_and_translation_invariance():
     assert np.array_equal(ft[sure], f0[sure])
 
 
+def test_tiny_scales_keep_the_verdict():
+    """Hexes scaled by 2^-340 .. 2^-360 (Bezier coefficients down to ~2^-1080, subnormal or
+    below: their high words no longer carry the sign of tiny positive values).  An
+    exact power-of-two scaling does not change any exact sign, so the verdict must equal the
+    oracle's on the unscaled hex; the subdivision kernel normalises such roots before splitting.
+    The SUBDIVIDED bit may differ (pass 1 cannot confirm Step 4 on subnormal coefficients)."""
+    base = hexgen.soa_config(3000, 0.35, 71)
+    ref = oracle.check_soa(base)
+    sure = ref["near"] == 0
+    cube = hexgen.nodes_to_soa(pins.KAPPA.astype(float)[None])
+    for e in (-340, -352, -360):
+        f, _ = gpu_soa(np.ldexp(base, e))
+        assert np.array_equal((f & 3)[sure], (ref["flags"] & 3)[sure]), e
+        fc, _ = gpu_soa(np.ldexp(cube, e))
+        assert (fc[0] & 3) == hv.VALID, (e, fc[0])
+
+
 def test_node_relabelling_by_cube_rotation_preserves_verdict():
     """A proper rotation of the reference cube relabels the nodes (det J composed with an
     orientation-preserving map of [0,1]^3): validity is unchanged."""
