@@ -744,8 +744,13 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
 // squared edge lengths), so only the winner takes a division and a sqrt.
 // ---------------------------------------------------------------------------
 
+#ifndef HEXVAL_QUALITY_MINB
+#define HEXVAL_QUALITY_MINB 3
+#endif
+constexpr int QUALITY_MINB = HEXVAL_QUALITY_MINB;   // 3: 80 registers (24 warps/SM): 304 us on config 1 vs 328 us at 2 (128 registers, no spills)
+
 template <class L>
-__global__ void __launch_bounds__(256, 2) quality_kernel(L ld, int64_t n, double* __restrict__ sj_out,
+__global__ void __launch_bounds__(256, QUALITY_MINB) quality_kernel(L ld, int64_t n, double* __restrict__ sj_out,
                                                        uint8_t* __restrict__ t1_out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
