@@ -111,7 +111,8 @@ struct IdxLoader {
     static constexpr bool kIntStep2 = true;      // see step2_class
     const double* __restrict__ verts;
     const int32_t* __restrict__ idx;
-    const uint8_t* dupf = nullptr;               // optional: precomputed duplicate-id flag of this thread's hex (smem)
+    uint32_t dupf = 0;                           // shared-memory address of this thread's precomputed duplicate-id
+                                                 // flag (the cp.async pipeline), else 0: re-read the ids
     __device__ __forceinline__ void load(int64_t i, double* X) const {
         int v[8];
         if ((((uintptr_t)idx) & 15) == 0) {
@@ -173,7 +174,11 @@ __device__ __forceinline__ bool ids_dup_face_pair(const int* v) {
 }
 
 __device__ __forceinline__ bool IdxLoader::dup_face_pair(int64_t i) const {
-    if (dupf) return *dupf != 0;
+    if (dupf) {
+        unsigned short f;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=h"(f) : "r"(dupf));
+        return f != 0;
+    }
     int v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = __ldg(idx + 8 * i + k);
@@ -720,7 +725,9 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
 #pragma unroll
             for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
 #ifndef HEXVAL_NO_DUPFLAG
-            st = body.hex(IdxLoader{verts, idx, bb ? dup1 : dup0}, X, i);
+            // the flag's 32-bit shared address, read on the slow path only (a generic pointer
+            // kept across the compute was spilled and its reload stalled: profiles/r02)
+            st = body.hex(IdxLoader{verts, idx, smem_u32(bb ? dup1 : dup0)}, X, i);
 #else
             st = body.hex(IdxLoader{verts, idx}, X, i);
 #endif
