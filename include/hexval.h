@@ -134,7 +134,9 @@ int hexval_classify_bezier(const double* coeffs, int64_t n, uint8_t* flags_out,
  *   sj_min_out_opt[i]  min over the 8 corners of the scaled Jacobian
  *                      det J / (|d_xi x| |d_eta x| |d_zeta x|) at the corner -- the
  *                      quality measure of PAPER.md:1212-1217 (Fig. 7: 0.64); NaN when a
- *                      corner edge has zero length or the hex is NONFINITE;
+ *                      corner edge has zero length or the hex is NONFINITE; valid over the
+ *                      whole input range (|x| <= 2^300: extreme edge scales are evaluated in
+ *                      a power-of-two rescaled frame, the measure being scale invariant);
  *   test1_out_opt[i]   1 iff det J > 0 at all 8 corners (Ushakova's Test 1, the 8 corner
  *                      tetrahedra: a necessary condition only, PAPER.md:107-109,
  *                      1260-1263), each sign exact: a corner sample within its fp64

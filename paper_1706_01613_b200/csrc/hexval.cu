@@ -338,8 +338,15 @@ __device__ __forceinline__ double len2(const V3& v) {
 // negative; T1_PENDING: some |c| <= tau2 (Step 2's rounding bound) and none
 // robustly negative -- the caller decides it in exact arithmetic (exact_test1).
 constexpr uint8_t T1_PENDING = 2;
+// or'ed into t1 when the hex's edge scale is outside [2^-64, 2^64): the products below
+// (squared-length products ~E^6, cross-multiplied ~E^12) could overflow or underflow,
+// so the caller recomputes sj in a power-of-two rescaled frame (corner_sj_rescaled)
+constexpr uint8_t SJ_RESCALE = 4;
 
-__device__ __forceinline__ void corner_quality(const V3* E, const double* c, int ekey, double& sj, uint8_t& t1) {
+__device__ __forceinline__ void corner_quality(const V3* E, const double* c, int ekey, double& sj, uint8_t& t1);
+
+// min corner scaled Jacobian from the 12 edge vectors and the 8 corner samples
+__device__ __forceinline__ double corner_sj(const V3* E, const double* c) {
     const double l12 = len2(E[0]), l43 = len2(E[1]), l56 = len2(E[2]), l87 = len2(E[3]);
     const double l14 = len2(E[4]), l23 = len2(E[5]), l58 = len2(E[6]), l67 = len2(E[7]);
     const double l15 = len2(E[8]), l26 = len2(E[9]), l48 = len2(E[10]), l37 = len2(E[11]);
@@ -347,16 +354,24 @@ __device__ __forceinline__ void corner_quality(const V3* E, const double* c, int
                          __dmul_rn(__dmul_rn(l43, l23), l37), __dmul_rn(__dmul_rn(l43, l14), l48),
                          __dmul_rn(__dmul_rn(l56, l58), l15), __dmul_rn(__dmul_rn(l56, l67), l26),
                          __dmul_rn(__dmul_rn(l87, l67), l37), __dmul_rn(__dmul_rn(l87, l58), l48)};
-    int km = key(c[0]);
     double bn = __dmul_rn(c[0], fabs(c[0])), bp = P[0], bc = c[0];
     bool zero_edge = !(P[0] > 0.0);
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
-        km = min(km, key(c[k]));
         zero_edge |= !(P[k] > 0.0);
         const double nk = __dmul_rn(c[k], fabs(c[k]));
         if (__dmul_rn(nk, bp) < __dmul_rn(bn, P[k])) { bn = nk; bp = P[k]; bc = c[k]; }   // nk/P[k] < bn/bp
     }
+    // the winner's c / sqrt(P) as c * rsqrt(P) (a few ulps; the parity tolerance is 1e-13)
+    return zero_edge ? __longlong_as_double(0x7ff8000000000000ll) : __dmul_rn(bc, rsqrt(bp));
+}
+
+__device__ __forceinline__ void corner_quality(const V3* E, const double* c, int ekey, double& sj, uint8_t& t1) {
+    const bool in_range = ekey >= 0x3BF00000 && ekey < 0x43F00000;   // 2^-64 <= E < 2^64
+    sj = corner_sj(E, c);                              // replaced by the rescaled value when !in_range
+    int km = key(c[0]);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) km = min(km, key(c[k]));
     const int T = key(step2_tau(ekey));                // tau2 > 0: key == abskey
     if (km > T) {
         t1 = 1;
@@ -366,8 +381,48 @@ __device__ __forceinline__ void corner_quality(const V3* E, const double* c, int
         for (int k = 1; k < 8; ++k) um = max(um, (unsigned)key(c[k]));
         t1 = um > (0x80000000u | (unsigned)T) ? 0 : T1_PENDING;   // a robustly negative corner, else exact
     }
-    // the winner's c / sqrt(P) as c * rsqrt(P) (a few ulps; the parity tolerance is 1e-13)
-    sj = zero_edge ? __longlong_as_double(0x7ff8000000000000ll) : __dmul_rn(bc, rsqrt(bp));
+    if (!in_range) t1 |= SJ_RESCALE;
+}
+
+// corner_sj for a hex whose edge scale is extreme: re-read the coordinates, scale the edge
+// vectors by 2^-e (E in [2^e, 2^(e+1)); exact) and recompute the 8 corner samples there --
+// the scaled Jacobian is invariant under the scaling.  Out of line (rare).
+template <class L>
+__device__ __forceinline__ double corner_sj_rescaled(const L& ld, int64_t i) {
+    double X[24];
+    ld.load(i, X);
+    V3 E[12];
+    {
+        const V3 n1{X[0], X[1], X[2]}, n2{X[3], X[4], X[5]}, n3{X[6], X[7], X[8]}, n4{X[9], X[10], X[11]};
+        const V3 n5{X[12], X[13], X[14]}, n6{X[15], X[16], X[17]}, n7{X[18], X[19], X[20]}, n8{X[21], X[22], X[23]};
+        E[0] = vsub(n2, n1); E[1] = vsub(n3, n4); E[2] = vsub(n6, n5); E[3] = vsub(n7, n8);
+        E[4] = vsub(n4, n1); E[5] = vsub(n3, n2); E[6] = vsub(n8, n5); E[7] = vsub(n7, n6);
+        E[8] = vsub(n5, n1); E[9] = vsub(n6, n2); E[10] = vsub(n8, n4); E[11] = vsub(n7, n3);
+    }
+    int ek = 0;
+    for (int q = 0; q < 12; ++q) ek = max(ek, max(abskey(E[q].x), max(abskey(E[q].y), abskey(E[q].z))));
+    const int e = max((ek >> 20) - 1023, -1022);
+    const double f = __hiloint2double((1023 - e) << 20, 0);          // 2^-e
+    for (int q = 0; q < 12; ++q) E[q] = {__dmul_rn(E[q].x, f), __dmul_rn(E[q].y, f), __dmul_rn(E[q].z, f)};
+    const double c[8] = {det3(E[0], E[4], E[8]), det3(E[0], E[5], E[9]), det3(E[1], E[5], E[11]),
+                         det3(E[1], E[4], E[10]), det3(E[2], E[6], E[8]), det3(E[2], E[7], E[9]),
+                         det3(E[3], E[7], E[11]), det3(E[3], E[6], E[10])};
+    return corner_sj(E, c);
+}
+
+// The rare paths of the NEXT-2 outputs in one out-of-line call (one call site per kernel
+// keeps the streaming kernels' register allocation unchanged): sj in a rescaled frame
+// (SJ_RESCALE) and Test 1 in exact arithmetic (T1_PENDING).
+struct QualOut {
+    double sj;
+    unsigned t1;
+};
+template <class L>
+__device__ __noinline__ QualOut quality_slow(const L ld, int64_t i, double sj, unsigned t1) {
+    if (t1 & SJ_RESCALE) sj = corner_sj_rescaled(ld, i);
+    t1 &= 3u;
+    if (t1 == T1_PENDING) t1 = exact_test1(ld, i);
+    return QualOut{sj, t1};
 }
 
 // S1-S5 + S8 for one hex whose 24 coordinates are in registers; returns the
@@ -392,7 +447,11 @@ __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i
         transform(s, t);                                  // S4 (Step 3)
         if (st == ST_VALID && !step4_positive(t)) st = ST_SUB;   // S5 (Step 4)
         if (COEFFS) write_coeffs(coeffs, n, i, s, t);
-        if (QUAL && t1 == T1_PENDING) t1 = exact_test1(ld, i);
+        if (QUAL && (t1 & (SJ_RESCALE | T1_PENDING))) {
+            const QualOut q = quality_slow(ld, i, sj, t1);
+            sj = q.sj;
+            t1 = (uint8_t)q.t1;
+        }
     }
     uint8_t f;
     switch (st) {
@@ -779,7 +838,11 @@ __global__ void __launch_bounds__(256, QUALITY_MINB) quality_kernel(L ld, int64_
 #pragma unroll
         for (int q = 0; q < 12; ++q) ek = max(ek, max(abskey(E[q].x), max(abskey(E[q].y), abskey(E[q].z))));
         corner_quality(E, c, ek, sj, t1);
-        if (t1 == T1_PENDING) t1 = exact_test1(ld, i);
+        if (t1 & (SJ_RESCALE | T1_PENDING)) {
+            const QualOut q = quality_slow(ld, i, sj, t1);
+            sj = q.sj;
+            t1 = (uint8_t)q.t1;
+        }
     }
     if (sj_out) __stcs(sj_out + i, sj);
     if (t1_out) __stcs(t1_out + i, t1);

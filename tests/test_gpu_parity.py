@@ -672,6 +672,25 @@ def test_corner_quality_special_cases(golden_hexes):
     _quality_parity(coords, sj, t1)
 
 
+@pytest.mark.parametrize("e", [-250, -100, -70, 70, 100, 250])
+def test_corner_quality_at_extreme_scales(e):
+    """The scaled Jacobian is scale invariant and Test 1 is a sign: at coordinate scales 2^e
+    where the squared-length products would overflow or underflow, the kernels recompute sj in
+    a power-of-two rescaled frame; both outputs equal the oracle's on the scaled hexes (and
+    the unscaled values), standalone and fused."""
+    coords = np.ldexp(hexgen.ragged_soa(3001, seed=77, amp=0.45), e)
+    dev = torch.from_numpy(coords).cuda()
+    sj, t1 = hv.corner_quality_soa(dev)
+    _, sj2, t12 = hv.check_screen_soa(dev)
+    torch.cuda.synchronize()
+    ref = _quality_parity(coords, sj.cpu().numpy(), t1.cpu().numpy())
+    _quality_parity(coords, sj2.cpu().numpy(), t12.cpu().numpy())
+    base = oracle.corner_quality_soa(np.ldexp(coords, -e))
+    ok = ~np.isnan(base["sj_min"])
+    assert np.max(np.abs(ref["sj_min"][ok] - base["sj_min"][ok]), initial=0.0) <= 1e-14
+    assert np.array_equal(ref["test1"], base["test1"])
+
+
 @pytest.mark.parametrize("n", [1, 255, 257, 256 * 148 * 2 + 77])
 def test_fused_screen_equals_separate_calls(n):
     """hexval_check_screen_soa: flags bit-identical to check_soa, sj/test1 bit-identical to
