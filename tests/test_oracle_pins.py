@@ -613,3 +613,16 @@ def test_quad_brute_force_and_exact_orientation():
             assert oracle.exact_orient2d(p, q, s) == (ex > 0) - (ex < 0)
     Q = SQ.copy(); Q[2] = [1.0, 0.0]                             # node 3 on node 2: J2 = J3 = 0 exactly
     assert oracle.check_quad(Q)["flags"] == oracle.INVALID
+
+
+def test_corner_quality_indexed_driver_equals_soa_driver():
+    """The indexed batch driver gathers the same 8 nodes as the SoA one (config-3 candidates,
+    duplicates included): identical outputs."""
+    verts, idx = hexgen.indexed_config(3, start=123, count=3000)
+    a = oracle.corner_quality_indexed(verts, idx)
+    b = oracle.corner_quality_soa(hexgen.indexed_to_soa(verts, idx))
+    for k in ("test1", "near"):
+        assert np.array_equal(a[k], b[k])
+    assert np.array_equal(np.isnan(a["sj_min"]), np.isnan(b["sj_min"]))
+    ok = ~np.isnan(a["sj_min"])
+    assert np.array_equal(a["sj_min"][ok], b["sj_min"][ok])
