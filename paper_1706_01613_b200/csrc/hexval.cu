@@ -896,11 +896,28 @@ struct WarpStacks {
 };
 
 // 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256): a node is 7 of them.
+#if defined(HEXVAL_K4_LD_DEFAULT)
+#define HV_LD_V4 "ld.global.v4.f64"
+#elif defined(HEXVAL_K4_LD_L1LAST)
+#define HV_LD_V4 "ld.global.L1::evict_last.v4.f64"
+#else
+#define HV_LD_V4 "ld.global.L1::evict_first.v4.f64"
+#endif
 __device__ __forceinline__ void ld_v4(const double* p, double& a, double& b, double& c, double& d) {
-    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p) : "memory");
+    asm volatile(HV_LD_V4 " {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p) : "memory");
 }
+// L1 policy of the stack traffic (measured on config 4, profiles/r02/K4_EXPERIMENTS.md): pushes
+// keep their lines in L1 (a pop on the same SM follows soon), popped lines are dead -- evict
+// them first: 267 ms vs 270 ms with default policies, 279 ms with no-allocate stores
+#if defined(HEXVAL_K4_ST_L1NOALLOC)
+#define HV_ST_V4 "st.global.L1::no_allocate.v4.f64"
+#elif defined(HEXVAL_K4_ST_DEFAULT)
+#define HV_ST_V4 "st.global.v4.f64"
+#else
+#define HV_ST_V4 "st.global.L1::evict_last.v4.f64"
+#endif
 __device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
-    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+    asm volatile(HV_ST_V4 " [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
 // A node on the stack: 7 x 32-byte vectors per slot, coalesced over the warp's
