@@ -71,6 +71,13 @@ constexpr int K4_MINB = HEXVAL_K4_MINB;
 #else
 #define HV_K4_BOUNDS __launch_bounds__(K4_THREADS, K4_MINB)
 #endif
+// The subdivision kernel with its node's xi split parked in tensor memory
+// (HEXVAL_K4_TMEM): 3 blocks of 4 warps per SM (<= 168 registers)
+#ifdef HEXVAL_K4_TMEM
+#define HV_SUBDIV_BOUNDS __launch_bounds__(K4_THREADS, 3)
+#else
+#define HV_SUBDIV_BOUNDS HV_K4_BOUNDS
+#endif
 
 // flags placeholders written by pass 1 for hexes that later kernels finish
 constexpr uint8_t PENDING_EXACT = 0xFF;
@@ -1078,11 +1085,141 @@ __device__ __forceinline__ void split_quarter_s(const double* G1, int hx, int hy
 }
 
 
+// ---- tensor memory as a per-thread scratchpad (HEXVAL_K4_TMEM) -----------
+// In the 32x32b shape thread t of warp w reads and writes TMEM lane
+// 32 (w mod 4) + t: a lane-private array of 32-bit columns.  K4 parks a node's
+// 45-value xi split there (90 columns, column-major by xi position a:
+// col = 18 a + 2 (j + 3 k)) and reads back one 9-value column per eta split, so
+// the split's live set drops from 45 + 45 to 9 + 45 values.
+#define HV_TM_ST(n, ...) asm volatile("tcgen05.st.sync.aligned.32x32b.x" #n ".b32 [%0], {" __VA_ARGS__ "};"
+struct TmemG1 {
+    uint32_t taddr;          // this warp's lane quarter, column 0 of the block's allocation
+    __device__ __forceinline__ void store(const double* G1) const {
+        uint32_t w[90];
+#pragma unroll
+        for (int a = 0; a < 5; ++a)
+#pragma unroll
+            for (int jk = 0; jk < 9; ++jk) {
+                const double v = G1[a + 5 * (jk % 3) + 15 * (jk / 3)];
+                w[18 * a + 2 * jk] = (uint32_t)__double2loint(v);
+                w[18 * a + 2 * jk + 1] = (uint32_t)__double2hiint(v);
+            }
+#pragma unroll
+        for (int c = 0; c < 80; c += 16)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                         ::"r"(taddr + c), "r"(w[c]), "r"(w[c + 1]), "r"(w[c + 2]), "r"(w[c + 3]), "r"(w[c + 4]),
+                         "r"(w[c + 5]), "r"(w[c + 6]), "r"(w[c + 7]), "r"(w[c + 8]), "r"(w[c + 9]), "r"(w[c + 10]),
+                         "r"(w[c + 11]), "r"(w[c + 12]), "r"(w[c + 13]), "r"(w[c + 14]), "r"(w[c + 15]) : "memory");
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + 80),
+                     "r"(w[80]), "r"(w[81]), "r"(w[82]), "r"(w[83]), "r"(w[84]), "r"(w[85]), "r"(w[86]), "r"(w[87])
+                     : "memory");
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr + 88), "r"(w[88]), "r"(w[89])
+                     : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    // column a of the xi split: g[j + 3k] = G1[a + 5j + 15k]
+    __device__ __forceinline__ void load_column(int a, double* g) const {
+        uint32_t w[18];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+                       "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]),
+                       "=r"(w[15])
+                     : "r"(taddr + 18 * a) : "memory");
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(w[16]), "=r"(w[17])
+                     : "r"(taddr + 18 * a + 16) : "memory");
+        // the wait names the destination registers so that no use is scheduled above it
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]),
+                       "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]), "+r"(w[12]), "+r"(w[13]), "+r"(w[14]),
+                       "+r"(w[15]), "+r"(w[16]), "+r"(w[17])
+                     :: "memory");
+#pragma unroll
+        for (int jk = 0; jk < 9; ++jk) g[jk] = __hiloint2double((int)w[2 * jk + 1], (int)w[2 * jk]);
+    }
+};
+#undef HV_TM_ST
+
+// split_quarter_s with the xi split read back from tensor memory column by column
+__device__ __forceinline__ void split_quarter_tm(const TmemG1& tm, int hx, int hy, const SplitScale& sc, double* Z) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double g[9];                                     // g[j + 3k]: column 2hx + a of the xi split
+        tm.load_column(2 * hx + a, g);
+        double B[9];                                     // B[u + 3k]: eta half hy of the column
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double s01, sm, s12;
+            line_split_s(g[3 * k], g[1 + 3 * k], g[2 + 3 * k], sc.r01[1], sc.r21[1], s01, sm, s12);
+            if (hy == 0) { B[3 * k] = g[3 * k]; B[1 + 3 * k] = s01; B[2 + 3 * k] = sm; }
+            else { B[3 * k] = sm; B[1 + 3 * k] = s12; B[2 + 3 * k] = g[2 + 3 * k]; }
+        }
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            double s01, sm, s12;
+            line_split_s(B[u], B[u + 3], B[u + 6], sc.r01[2], sc.r21[2], s01, sm, s12);
+            double* z = Z + a + 3 * u;
+            z[0] = B[u]; z[9] = s01; z[18] = sm; z[27] = s12; z[36] = B[u + 6];
+        }
+    }
+}
+
+struct TmemBlock {           // the block's TMEM allocation (one warp allocates and frees)
+    static constexpr int COLS = 128;
+    __device__ __forceinline__ static uint32_t alloc(uint32_t* slot) {
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+                         "n"(COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        return *((volatile uint32_t*)slot);
+    }
+    __device__ __forceinline__ static void free(uint32_t base) {
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(COLS));
+    }
+};
+
 struct K4Warp {
     unsigned status[32];    // per batch slot: bit 0 INVALID found, bit 1 depth cap reached
     uint32_t hex[32];       // hex id of each batch slot
-    int cnt[MAX_DEPTH + 1]; // nodes per level on the stack
 };
+
+// Per-level node counts of a warp's depth-sorted stack, kept in registers: the
+// top level's count warp-uniform (tcnt), the count of each level L below it in
+// lane L (lcnt; 0 for empty levels and for the top level and above).  A step's
+// pop size is then known without a shared-memory round trip, and the next
+// nonempty level is one ballot away (profiles/r02/K4_EXPERIMENTS.md: the
+// shared-memory counters' load-use chains were 8% of the kernel's stall samples).
+struct LevelCounts {
+    int tcnt = 0, lcnt = 0;
+    // after a step at level d (the top level) that pushed `pushed` nodes at level d+1
+    __device__ __forceinline__ void after_step(int lane, int d, int pushed, int& D) {
+        if (pushed) {
+            if (lane == d) lcnt = tcnt;                   // level d keeps what was not popped
+            tcnt = pushed;
+            D = d + 1;
+        } else if (tcnt == 0) {
+            const unsigned ne = __ballot_sync(0xffffffffu, lcnt > 0);   // nonempty levels below d
+            D = ne ? 31 - __clz(ne) : 0;
+            tcnt = __shfl_sync(0xffffffffu, lcnt, D);
+            if (lane == D) lcnt = 0;
+        }
+    }
+};
+
+// 32-bit shared-memory load that the compiler keeps where it is written: the
+// status of a popped node's hex is read after the xi split, off the pop's
+// load-use chain
+__device__ __forceinline__ unsigned ld_shared_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
 
 // Root coefficients of queued item h: recomputed from the coordinates with
 // the pass-1 arithmetic, or read from caller-supplied Bezier coefficients
@@ -1147,7 +1284,7 @@ struct CoeffRoot {
 };
 
 template <class R, bool STATS>
-__global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
+__global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
                                                             const uint32_t* __restrict__ qsub,
                                                             const uint32_t* __restrict__ qexact, WarpStacks ws,
                                                             hexval_stats* stats) {
@@ -1156,12 +1293,17 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
     K4Warp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
     double* const sc = ws.coef + gw * 28 * K4_CAP;
+#ifdef HEXVAL_K4_TMEM
+    static_assert(K4_THREADS == 128, "one warp per TMEM lane quarter");
+    __shared__ uint32_t tmem_slot;
+    const uint32_t tmem_base = TmemBlock::alloc(&tmem_slot);
+    const TmemG1 tm{tmem_base + ((uint32_t)(32 * (threadIdx.x >> 5)) << 16)};
+#endif
     const unsigned total = *((volatile unsigned*)&ctl->n_sub);
     const unsigned n_exact = *((volatile unsigned*)&ctl->n_exact);
     bool ex_left = n_exact > 0;                          // warp-uniform: the exact queue may hold items
     const unsigned lt_mask = (1u << lane) - 1u;
-    if (lane <= MAX_DEPTH) W.cnt[lane] = 0;
-    __syncwarp();
+    LevelCounts lc;
     int top = 0, D = 0, nb = 0;                         // warp-uniform: stack size, top level, batch size
     unsigned long long nodes = 0, n_inv = 0, n_val = 0, n_und = 0, n_ex = 0, n_exi = 0, n_exv = 0, steps = 0;
     int maxd = 0;
@@ -1216,37 +1358,54 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             }
             __syncwarp();
             if (nb == 0) break;
-            act = lane < nb;
-            d = 0;
-            if (act) {
+            // the batch's roots (pass 1's arithmetic, normalised if extreme) go onto the
+            // stack as level 0, so that every step takes its nodes from one place
+            if (lane < nb) {
                 W.status[lane] = 0;
-                root(W.hex[lane], P);                    // pass 1's root (normalised if extreme)
+                double R[27];
+                root(W.hex[lane], R);
+                stack_store(sc, lane, R, (unsigned long long)(unsigned)lane | ((unsigned long long)ROOT_PATTERN << 32));
             }
-        } else {
-            const int k = min(32, W.cnt[D]);
-            HV_CHECK(D > 0 && D < MAX_DEPTH && k > 0 && k <= top);
+            top = nb;
+            lc.tcnt = nb;
+            D = 0;
+            __syncwarp();
+        }
+        {
+            const int k = min(32, lc.tcnt);
+            HV_CHECK(D >= 0 && D < MAX_DEPTH && k > 0 && k <= top);
             act = lane < k;
             d = D;
-            if (act) {
-                const int slot = top - k + lane;
+            {
+                // lanes >= k load the last popped node again (same lines, no extra traffic)
+                // and drop it: an unconditional load keeps P out of a divergent merge
+                const int slot = top - k + min(lane, k - 1);
                 const unsigned long long meta = stack_load(sc, slot, P);
                 owner = (int)(unsigned)meta;
                 pat = (unsigned)(meta >> 32);
-                act = (W.status[owner] & 1u) == 0;       // hex already INVALID: drop the node
             }
             top -= k;
-            __syncwarp();
-            if (lane == 0) W.cnt[D] -= k;
+            lc.tcnt -= k;
         }
-        __syncwarp();
-        const unsigned actmask = __ballot_sync(0xffffffffu, act);
-        if (STATS && actmask) { nodes += __popc(actmask); maxd = max(maxd, d + 1); }
-        if (STATS) ++steps;
         // ---- split every active node into its 8 children --------------------
         SplitScale ss;
         ss.unpack(pat);
+#ifdef HEXVAL_K4_TMEM
+        {
+            double G1[45];
+            split_xi_s(P, ss, G1);
+            tm.store(G1);
+        }
+#else
         double G1[45];
         split_xi_s(P, ss, G1);
+#endif
+        if (d > 0 && act) act = (ld_shared_u32(&W.status[owner]) & 1u) == 0;   // hex already INVALID: drop the node
+        if (STATS) {
+            const unsigned actmask = __ballot_sync(0xffffffffu, act);
+            if (actmask) { nodes += __popc(actmask); maxd = max(maxd, d + 1); }
+            ++steps;
+        }
         bool inval = false, capped = false;
         int pushed = 0;                                  // warp-uniform
         const bool can_push = d + 1 < MAX_DEPTH;
@@ -1255,7 +1414,11 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
 #pragma unroll
             for (int hy = 0; hy < 2; ++hy) {
                 double Z[45];
+                #ifdef HEXVAL_K4_TMEM
+                split_quarter_tm(tm, hx, hy, ss, Z);
+#else
                 split_quarter_s(G1, hx, hy, ss, Z);
+#endif
                 // classify the two children (zeta halves hz = 0, 1) from per-plane key
                 // minima: planes v = 0, 2, 4 split into their 4 corners and 5 others,
                 // planes 1 and 3 lie inside both children
@@ -1312,13 +1475,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
         if (inval) atomicOr(&W.status[owner], 1u);
         if (capped) atomicOr(&W.status[owner], 2u);
         top += pushed;
-        __syncwarp();
-        if (pushed) {
-            if (lane == 0) W.cnt[d + 1] += pushed;
-            D = d + 1;
-        } else {
-            while (D > 0 && W.cnt[D] == 0) --D;           // W.cnt[D] was updated by lane 0 before the sync
-        }
+        lc.after_step(lane, d, pushed, D);
         __syncwarp();
     }
     if (STATS) {
@@ -1350,6 +1507,9 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             }
         }
     }
+#ifdef HEXVAL_K4_TMEM
+    TmemBlock::free(tmem_base);
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1852,6 +2012,11 @@ const DeviceInfo& device_info(int dev) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false>, K4_THREADS,
                                                       0);
         d.k4_blocks_per_sm = occ > 0 ? occ : 1;
+#ifdef HEXVAL_K4_TMEM
+        // the occupancy calculator assumes a tcgen05.alloc kernel may hold the whole
+        // 512-column TMEM and reports 1 block/SM; 3 blocks x 128 columns fit
+        d.k4_blocks_per_sm = 3;
+#endif
         const int want = pass1_variant_from_env();
         const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup() : 0);
         d.p1_variant = ctas > 0 ? want : P1_LDG;
