@@ -626,6 +626,13 @@ __global__ void __launch_bounds__(WT_THREADS, 2)
 constexpr int CP_THREADS = HEXVAL_CP_THREADS;        // A/B builds: 128 x 4 or 256 x 2 CTAs/SM (16 warps/SM)
 constexpr int CP_MINB = 512 / CP_THREADS;
 constexpr size_t CP_SMEM = (size_t)2 * 24 * CP_THREADS * sizeof(double);   // 96 KB: two tiles
+// The fused validity + screening pass (QUAL bodies) carries more live state per hex: it runs
+// with its own block size (A/B knob; 384 x 1 = 12 warps/SM at <= 168 registers).
+#ifndef HEXVAL_SCREEN_THREADS
+#define HEXVAL_SCREEN_THREADS 384
+#endif
+template <int T> constexpr size_t cp_smem() { return (size_t)2 * 24 * T * sizeof(double); }
+template <int T> constexpr int cp_minb() { return T >= 512 ? 1 : 512 / T; }
 
 __device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, uint64_t policy) {
     asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "l"(policy)
@@ -634,11 +641,12 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, uint6
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
+template <int T>
 __device__ __forceinline__ void cp_issue_hex(const double* __restrict__ coords, int64_t n, int64_t i, uint32_t dst) {
     if (i < n) {
         const uint64_t policy = policy_evict_first();
 #pragma unroll
-        for (int p = 0; p < 24; ++p) cp_async8(dst + p * CP_THREADS * 8, coords + (int64_t)p * n + i, policy);
+        for (int p = 0; p < 24; ++p) cp_async8(dst + p * T * 8, coords + (int64_t)p * n + i, policy);
     }
     cp_async_commit();                                        // (possibly empty) group per tile
 }
@@ -648,6 +656,8 @@ __device__ __forceinline__ void cp_issue_hex(const double* __restrict__ coords, 
 // (every lane, st = -1 without a hex); finish() once per thread at the end.
 template <bool COEFFS, bool STATS, bool QUAL = false>
 struct Pass1Body {                                           // K1/K2: S1-S8 + K3 (+ NEXT-2 outputs)
+    static constexpr int THREADS = QUAL ? HEXVAL_SCREEN_THREADS : CP_THREADS;
+    static constexpr int MINB = cp_minb<THREADS>();
     int64_t n;
     uint8_t* flags;
     double* coeffs;
@@ -672,8 +682,9 @@ struct Pass1Body {                                           // K1/K2: S1-S8 + K
 };
 
 template <class Body>
-__global__ void __launch_bounds__(CP_THREADS, CP_MINB)
+__global__ void __launch_bounds__(Body::THREADS, Body::MINB)
     soa_cp_kernel(const double* __restrict__ coords, int64_t n, Body body) {
+    constexpr int CP_THREADS = Body::THREADS;
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS]
     const int tid = threadIdx.x;
     // 32-bit tile counters (n <= INT32_MAX): loop state that fits one register each, so the
@@ -688,8 +699,8 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
     const uint32_t s0 = smem_u32(cp_buf + tid);
     const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
     tile_t t = blockIdx.x;
-    cp_issue_hex(coords, n, (int64_t)t * CP_THREADS + tid, s0);
-    cp_issue_hex(coords, n, (int64_t)(t + G) * CP_THREADS + tid, s1);
+    cp_issue_hex<CP_THREADS>(coords, n, (int64_t)t * CP_THREADS + tid, s0);
+    cp_issue_hex<CP_THREADS>(coords, n, (int64_t)(t + G) * CP_THREADS + tid, s1);
     for (int k = 0; t < tiles; t += G, ++k) {
         const int b = k & 1;
         cp_async_wait1();                                    // tile k has landed (tile k+1 may be in flight)
@@ -703,7 +714,7 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
             st = body.hex(SoaLoader{coords, n}, X, i);
         }
         // refill this buffer with tile k+2 (X was consumed above: program order)
-        cp_issue_hex(coords, n, (int64_t)(t + 2 * G) * CP_THREADS + tid, b ? s1 : s0);
+        cp_issue_hex<CP_THREADS>(coords, n, (int64_t)(t + 2 * G) * CP_THREADS + tid, b ? s1 : s0);
         body.epilogue(st, i);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -718,6 +729,7 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
 // after computing, the thread reads that row from shared memory and issues the
 // gathers of tile k+2.  No register holds prefetched data across the compute.
 constexpr size_t CPI_SMEM = CP_SMEM + (size_t)2 * CP_THREADS * 32 + (size_t)2 * CP_THREADS;   // + two idx tiles, two dup-flag tiles
+template <int T> constexpr size_t cpi_smem() { return cp_smem<T>() + (size_t)2 * T * 32 + (size_t)2 * T; }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
@@ -730,6 +742,7 @@ __device__ __forceinline__ void cp_idx_row(const int32_t* __restrict__ idx, int6
     }
 }
 
+template <int CP_THREADS>
 __device__ __forceinline__ void cp_gather_row(const double* __restrict__ verts, int64_t n, int64_t i,
                                               const int32_t* row, uint32_t dst, uint8_t* dupf) {
     if (i < n) {
@@ -753,8 +766,9 @@ __device__ __forceinline__ void cp_gather_row(const double* __restrict__ verts, 
 }
 
 template <class Body>
-__global__ void __launch_bounds__(CP_THREADS, CP_MINB)
+__global__ void __launch_bounds__(Body::THREADS, Body::MINB)
     idx_cp_kernel(const double* __restrict__ verts, const int32_t* __restrict__ idx, int64_t n, Body body) {
+    constexpr int CP_THREADS = Body::THREADS;
     extern __shared__ __align__(128) double cp_buf[];        // [2][24][CP_THREADS] coords, then [2][CP_THREADS][8] ids
     const int tid = threadIdx.x;
     const int tiles = (int)((n + CP_THREADS - 1) / CP_THREADS);   // 32-bit loop state (see soa_cp_kernel)
@@ -774,10 +788,10 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
     cp_idx_row(idx, n, hex_of(t), r0);
     cp_idx_row(idx, n, hex_of(t + G), r1);
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    cp_gather_row(verts, n, hex_of(t), row0, s0, dup0);
+    cp_gather_row<CP_THREADS>(verts, n, hex_of(t), row0, s0, dup0);
     cp_idx_row(idx, n, hex_of(t + 2 * G), r0);
     cp_async_commit();
-    cp_gather_row(verts, n, hex_of(t + G), row1, s1, dup1);
+    cp_gather_row<CP_THREADS>(verts, n, hex_of(t + G), row1, s1, dup1);
     cp_idx_row(idx, n, hex_of(t + 3 * G), r1);
     cp_async_commit();
     for (int k = 0; t < tiles; t += G, ++k) {
@@ -799,7 +813,7 @@ __global__ void __launch_bounds__(CP_THREADS, CP_MINB)
 #endif
         }
         // group k+2: gathers of tile k+2 (row read from shared memory), row of tile k+4
-        cp_gather_row(verts, n, hex_of(t + 2 * G), bb ? row1 : row0, bb ? s1 : s0, bb ? dup1 : dup0);
+        cp_gather_row<CP_THREADS>(verts, n, hex_of(t + 2 * G), bb ? row1 : row0, bb ? s1 : s0, bb ? dup1 : dup0);
         cp_idx_row(idx, n, hex_of(t + 4 * G), bb ? r1 : r0);
         cp_async_commit();
         body.epilogue(st, i);
@@ -1087,46 +1101,59 @@ __device__ __forceinline__ void split_quarter_s(const double* G1, int hx, int hy
 
 // ---- tensor memory as a per-thread scratchpad (HEXVAL_K4_TMEM) -----------
 // In the 32x32b shape thread t of warp w reads and writes TMEM lane
-// 32 (w mod 4) + t: a lane-private array of 32-bit columns.  K4 parks a node's
-// 45-value xi split there (90 columns, column-major by xi position a:
-// col = 18 a + 2 (j + 3 k)) and reads back one 9-value column per eta split, so
-// the split's live set drops from 45 + 45 to 9 + 45 values.
-#define HV_TM_ST(n, ...) asm volatile("tcgen05.st.sync.aligned.32x32b.x" #n ".b32 [%0], {" __VA_ARGS__ "};"
-struct TmemG1 {
+// 32 (w mod 4) + t: a lane-private array of 32-bit columns.  K4 parks the
+// node's xi split there -- the five xi positions a as 9-value columns
+// g[j + 3k] -- and reads one column back per eta split, so the split's live
+// set drops from 45 + 45 to 9 + 45 values and 3 blocks of 4 warps fit an SM.
+// Nodes on the stack are i-major in this build (NI), so that the two xi
+// positions a = 0, 4 of a popped node are contiguous runs of its vectors.
+// Columns (32-bit): a0 -> 0, a4 -> 18, a1 (s01) -> 36, a2 (sm) -> 54,
+// a3 (s12) -> 72; each eta split's second half (hy = 1) is parked in a column
+// that is dead by then (hx = 0: 0, 36, 90; hx = 1: 54, 72, 18).
+#ifdef HEXVAL_K4_TMEM
+__host__ __device__ constexpr int NI(int i, int j, int k) { return 9 * i + j + 3 * k; }
+#else
+__host__ __device__ constexpr int NI(int i, int j, int k) { return i + 3 * j + 9 * k; }
+#endif
+struct TmemSplit {
     uint32_t taddr;          // this warp's lane quarter, column 0 of the block's allocation
-    __device__ __forceinline__ void store(const double* G1) const {
-        uint32_t w[90];
-#pragma unroll
-        for (int a = 0; a < 5; ++a)
-#pragma unroll
-            for (int jk = 0; jk < 9; ++jk) {
-                const double v = G1[a + 5 * (jk % 3) + 15 * (jk / 3)];
-                w[18 * a + 2 * jk] = (uint32_t)__double2loint(v);
-                w[18 * a + 2 * jk + 1] = (uint32_t)__double2hiint(v);
-            }
-#pragma unroll
-        for (int c = 0; c < 80; c += 16)
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-                         ::"r"(taddr + c), "r"(w[c]), "r"(w[c + 1]), "r"(w[c + 2]), "r"(w[c + 3]), "r"(w[c + 4]),
-                         "r"(w[c + 5]), "r"(w[c + 6]), "r"(w[c + 7]), "r"(w[c + 8]), "r"(w[c + 9]), "r"(w[c + 10]),
-                         "r"(w[c + 11]), "r"(w[c + 12]), "r"(w[c + 13]), "r"(w[c + 14]), "r"(w[c + 15]) : "memory");
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + 80),
-                     "r"(w[80]), "r"(w[81]), "r"(w[82]), "r"(w[83]), "r"(w[84]), "r"(w[85]), "r"(w[86]), "r"(w[87])
-                     : "memory");
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr + 88), "r"(w[88]), "r"(w[89])
-                     : "memory");
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    __device__ __forceinline__ static constexpr int COL(int a) { return a == 0 ? 0 : (a == 4 ? 18 : 18 + 18 * a); }
+    __device__ __forceinline__ static constexpr int PARK(int hx, int c) {
+        return hx == 0 ? (c == 0 ? 0 : (c == 1 ? 36 : 90)) : (c == 0 ? 54 : (c == 1 ? 72 : 18));
     }
-    // column a of the xi split: g[j + 3k] = G1[a + 5j + 15k]
-    __device__ __forceinline__ void load_column(int a, double* g) const {
+    // one 2-column store per double: a double is already an aligned register pair, so
+    // no register moves are needed to gather the 9 values into a 16-register block
+    __device__ __forceinline__ void put9(int col, const double* v) const {
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr + col + 2 * q),
+                         "r"(__double2loint(v[q])), "r"(__double2hiint(v[q])) : "memory");
+    }
+    // 2^n doubles (n = 0, 1, 2) from consecutive registers (e.g. one 256-bit stack vector)
+    template <int N>
+    __device__ __forceinline__ void putN(int col, const double* v) const {
+        if (N == 4)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + col),
+                         "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])),
+                         "r"(__double2hiint(v[1])), "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])),
+                         "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])) : "memory");
+        else if (N == 2)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr + col),
+                         "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])),
+                         "r"(__double2hiint(v[1])) : "memory");
+        else
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr + col),
+                         "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])) : "memory");
+    }
+    __device__ __forceinline__ void get9(int col, double* v) const {
         uint32_t w[18];
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
                        "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]),
                        "=r"(w[15])
-                     : "r"(taddr + 18 * a) : "memory");
+                     : "r"(taddr + col) : "memory");
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(w[16]), "=r"(w[17])
-                     : "r"(taddr + 18 * a + 16) : "memory");
+                     : "r"(taddr + col + 16) : "memory");
         // the wait names the destination registers so that no use is scheduled above it
         asm volatile("tcgen05.wait::ld.sync.aligned;"
                      : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]),
@@ -1134,32 +1161,63 @@ struct TmemG1 {
                        "+r"(w[15]), "+r"(w[16]), "+r"(w[17])
                      :: "memory");
 #pragma unroll
-        for (int jk = 0; jk < 9; ++jk) g[jk] = __hiloint2double((int)w[2 * jk + 1], (int)w[2 * jk]);
+        for (int q = 0; q < 9; ++q) v[q] = __hiloint2double((int)w[2 * q + 1], (int)w[2 * q]);
     }
+    __device__ __forceinline__ static void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 };
-#undef HV_TM_ST
 
-// split_quarter_s with the xi split read back from tensor memory column by column
-__device__ __forceinline__ void split_quarter_tm(const TmemG1& tm, int hx, int hy, const SplitScale& sc, double* Z) {
+// xi split of an i-major node into TMEM: the columns a = 0, 4 are the node's
+// own xi = 0, 2 slabs, a = 1, 2, 3 the scaled de Casteljau values of the 9 lines
+__device__ __forceinline__ void split_xi_tm(const double* P, const SplitScale& sc, const TmemSplit& tm) {
+    double s01[9], sm[9], s12[9];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        double g[9];                                     // g[j + 3k]: column 2hx + a of the xi split
-        tm.load_column(2 * hx + a, g);
-        double B[9];                                     // B[u + 3k]: eta half hy of the column
+    for (int q = 0; q < 9; ++q) line_split_s(P[q], P[9 + q], P[18 + q], sc.r01[0], sc.r21[0], s01[q], sm[q], s12[q]);
+    // the xi = 0, 2 slabs straight from the popped node's 256-bit vectors (P[0..3], P[4..7], ...)
+    // (a 256-bit load fills two 4-register groups: one 4-column store per group)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            double s01, sm, s12;
-            line_split_s(g[3 * k], g[1 + 3 * k], g[2 + 3 * k], sc.r01[1], sc.r21[1], s01, sm, s12);
-            if (hy == 0) { B[3 * k] = g[3 * k]; B[1 + 3 * k] = s01; B[2 + 3 * k] = sm; }
-            else { B[3 * k] = sm; B[1 + 3 * k] = s12; B[2 + 3 * k] = g[2 + 3 * k]; }
-        }
+    for (int q = 0; q < 8; q += 2) tm.putN<2>(TmemSplit::COL(0) + 2 * q, P + q);
+    tm.putN<1>(TmemSplit::COL(0) + 16, P + 8);
 #pragma unroll
-        for (int u = 0; u < 3; ++u) {
-            double s01, sm, s12;
-            line_split_s(B[u], B[u + 3], B[u + 6], sc.r01[2], sc.r21[2], s01, sm, s12);
-            double* z = Z + a + 3 * u;
-            z[0] = B[u]; z[9] = s01; z[18] = sm; z[27] = s12; z[36] = B[u + 6];
-        }
+    for (int q = 0; q < 8; q += 2) tm.putN<2>(TmemSplit::COL(4) + 2 * q, P + 18 + q);
+    tm.putN<1>(TmemSplit::COL(4) + 16, P + 26);
+    tm.put9(TmemSplit::COL(1), s01);
+    tm.put9(TmemSplit::COL(2), sm);
+    tm.put9(TmemSplit::COL(3), s12);
+    TmemSplit::wait_st();
+}
+
+// eta split of column c of xi half hx: half hy = 0 goes into the quarter Z (zeta
+// split, layout of split_quarter_s), half hy = 1 is parked in TMEM
+__device__ __forceinline__ void eta_zeta_tm(const TmemSplit& tm, int hx, int c, const SplitScale& sc, double* Z) {
+    double g[9];
+    tm.get9(TmemSplit::COL(2 * hx + c), g);
+    double B0[9], B1[9];                                 // B[u + 3k]
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double s01, sm, s12;
+        line_split_s(g[3 * k], g[1 + 3 * k], g[2 + 3 * k], sc.r01[1], sc.r21[1], s01, sm, s12);
+        B0[3 * k] = g[3 * k]; B0[1 + 3 * k] = s01; B0[2 + 3 * k] = sm;
+        B1[3 * k] = sm; B1[1 + 3 * k] = s12; B1[2 + 3 * k] = g[2 + 3 * k];
+    }
+    tm.put9(TmemSplit::PARK(hx, c), B1);
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+        double s01, sm, s12;
+        line_split_s(B0[u], B0[u + 3], B0[u + 6], sc.r01[2], sc.r21[2], s01, sm, s12);
+        double* z = Z + c + 3 * u;
+        z[0] = B0[u]; z[9] = s01; z[18] = sm; z[27] = s12; z[36] = B0[u + 6];
+    }
+}
+// the parked hy = 1 half of column c: zeta split into Z
+__device__ __forceinline__ void zeta_parked_tm(const TmemSplit& tm, int hx, int c, const SplitScale& sc, double* Z) {
+    double B1[9];
+    tm.get9(TmemSplit::PARK(hx, c), B1);
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+        double s01, sm, s12;
+        line_split_s(B1[u], B1[u + 3], B1[u + 6], sc.r01[2], sc.r21[2], s01, sm, s12);
+        double* z = Z + c + 3 * u;
+        z[0] = B1[u]; z[9] = s01; z[18] = sm; z[27] = s12; z[36] = B1[u + 6];
     }
 }
 
@@ -1297,7 +1355,7 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
     static_assert(K4_THREADS == 128, "one warp per TMEM lane quarter");
     __shared__ uint32_t tmem_slot;
     const uint32_t tmem_base = TmemBlock::alloc(&tmem_slot);
-    const TmemG1 tm{tmem_base + ((uint32_t)(32 * (threadIdx.x >> 5)) << 16)};
+    const TmemSplit tm{tmem_base + ((uint32_t)(32 * (threadIdx.x >> 5)) << 16)};
 #endif
     const unsigned total = *((volatile unsigned*)&ctl->n_sub);
     const unsigned n_exact = *((volatile unsigned*)&ctl->n_exact);
@@ -1362,9 +1420,15 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
             // stack as level 0, so that every step takes its nodes from one place
             if (lane < nb) {
                 W.status[lane] = 0;
-                double R[27];
+                double R[27], Rn[27];
                 root(W.hex[lane], R);
-                stack_store(sc, lane, R, (unsigned long long)(unsigned)lane | ((unsigned long long)ROOT_PATTERN << 32));
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) Rn[NI(i, j, k)] = R[i + 3 * j + 9 * k];   // the stack's node layout
+                stack_store(sc, lane, Rn, (unsigned long long)(unsigned)lane | ((unsigned long long)ROOT_PATTERN << 32));
             }
             top = nb;
             lc.tcnt = nb;
@@ -1391,11 +1455,7 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
         SplitScale ss;
         ss.unpack(pat);
 #ifdef HEXVAL_K4_TMEM
-        {
-            double G1[45];
-            split_xi_s(P, ss, G1);
-            tm.store(G1);
-        }
+        split_xi_tm(P, ss, tm);
 #else
         double G1[45];
         split_xi_s(P, ss, G1);
@@ -1409,16 +1469,8 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
         bool inval = false, capped = false;
         int pushed = 0;                                  // warp-uniform
         const bool can_push = d + 1 < MAX_DEPTH;
-#pragma unroll
-        for (int hx = 0; hx < 2; ++hx)
-#pragma unroll
-            for (int hy = 0; hy < 2; ++hy) {
-                double Z[45];
-                #ifdef HEXVAL_K4_TMEM
-                split_quarter_tm(tm, hx, hy, ss, Z);
-#else
-                split_quarter_s(G1, hx, hy, ss, Z);
-#endif
+        // classify and push the two children (zeta halves) of quarter (hx, hy)
+        auto quarter = [&](const int hx, const int hy, const double* Z) {
                 // classify the two children (zeta halves hz = 0, 1) from per-plane key
                 // minima: planes v = 0, 2, 4 split into their 4 corners and 5 others,
                 // planes 1 and 3 lie inside both children
@@ -1462,7 +1514,7 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
 #pragma unroll
                                 for (int u = 0; u < 3; ++u)
 #pragma unroll
-                                    for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
+                                    for (int a = 0; a < 3; ++a) C[NI(a, u, v)] = Z[a + 3 * u + 9 * (2 * hz + v)];
                             stack_store(sc, slot, C,
                                         (unsigned long long)(unsigned)owner |
                                             ((unsigned long long)ss.child(hx, hy, hz) << 32));
@@ -1471,7 +1523,29 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
                     }
                     pushed += c0 + __popc(b1);
                 }
+        };
+#ifdef HEXVAL_K4_TMEM
+#pragma unroll
+        for (int hx = 0; hx < 2; ++hx) {
+            double Z[45];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) eta_zeta_tm(tm, hx, c, ss, Z);
+            quarter(hx, 0, Z);
+            TmemSplit::wait_st();
+#pragma unroll
+            for (int c = 0; c < 3; ++c) zeta_parked_tm(tm, hx, c, ss, Z);
+            quarter(hx, 1, Z);
+        }
+#else
+#pragma unroll
+        for (int hx = 0; hx < 2; ++hx)
+#pragma unroll
+            for (int hy = 0; hy < 2; ++hy) {
+                double Z[45];
+                split_quarter_s(G1, hx, hy, ss, Z);
+                quarter(hx, hy, Z);
             }
+#endif
         if (inval) atomicOr(&W.status[owner], 1u);
         if (capped) atomicOr(&W.status[owner], 2u);
         top += pushed;
@@ -1940,6 +2014,7 @@ struct DeviceInfo {
     int k4_blocks_per_sm = 0;
     int p1_variant = 0;           // SoA pass 1: P1_LDG (plain), P1_WTMA or P1_CP
     int p1_ctas_per_sm = 1;
+    int screen_ctas_per_sm = 1;   // the fused screening pass (its own block size)
     bool ok = false;
 };
 
@@ -1966,28 +2041,31 @@ int wtma_setup() {
 }
 
 template <class Body>
-bool cp_attr(size_t smem_soa, size_t smem_idx) {
+bool cp_attr(size_t smem_soa = cp_smem<Body::THREADS>(), size_t smem_idx = cpi_smem<Body::THREADS>()) {
     return cudaFuncSetAttribute((const void*)soa_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem_soa) == cudaSuccess &&
            cudaFuncSetAttribute((const void*)idx_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem_idx) == cudaSuccess;
 }
 
-int cp_setup() {
+int cp_setup(int* screen_ctas) {
     const bool ok = cp_attr<Pass1Body<false, false>>(CP_SMEM, CPI_SMEM) && cp_attr<Pass1Body<false, true>>(CP_SMEM, CPI_SMEM) &&
                     cp_attr<Pass1Body<true, false>>(CP_SMEM, CPI_SMEM) && cp_attr<Pass1Body<true, true>>(CP_SMEM, CPI_SMEM) &&
-                    cp_attr<Pass1Body<false, false, true>>(CP_SMEM, CPI_SMEM) &&
-                    cp_attr<Pass1Body<false, true, true>>(CP_SMEM, CPI_SMEM);
+                    cp_attr<Pass1Body<false, false, true>>() && cp_attr<Pass1Body<false, true, true>>();
     if (!ok) {
         cudaGetLastError();
         return 0;
     }
-    int occ = 0;
+    int occ = 0, socc = 0;
+    using SB = Pass1Body<false, false, true>;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, soa_cp_kernel<Pass1Body<false, false>>, CP_THREADS,
-                                                      CP_SMEM) != cudaSuccess) {
+                                                      CP_SMEM) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&socc, soa_cp_kernel<SB>, SB::THREADS,
+                                                      cp_smem<SB::THREADS>()) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
+    *screen_ctas = socc > 0 ? socc : 1;
     return occ;
 }
 
@@ -2018,7 +2096,7 @@ const DeviceInfo& device_info(int dev) {
         d.k4_blocks_per_sm = 3;
 #endif
         const int want = pass1_variant_from_env();
-        const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup() : 0);
+        const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup(&d.screen_ctas_per_sm) : 0);
         d.p1_variant = ctas > 0 ? want : P1_LDG;
         d.p1_ctas_per_sm = ctas > 0 ? ctas : 1;
         d.ok = true;
@@ -2082,11 +2160,12 @@ void launch_pass1<IdxLoader>(const IdxLoader& ld, const DeviceInfo& info, const 
         launch_pass1_plain(ld, a, stream);
         return;
     }
-    const int64_t tiles = (a.n + CP_THREADS - 1) / CP_THREADS;
-    const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
-    const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
     with_pass1_body(a, [&](auto body) {
-        idx_cp_kernel<<<grid, CP_THREADS, CPI_SMEM, stream>>>(ld.verts, ld.idx, a.n, body);
+        constexpr int T = decltype(body)::THREADS;
+        const int64_t tiles = (a.n + T - 1) / T;
+        const int64_t cap = (int64_t)info.sms * (T == CP_THREADS ? info.p1_ctas_per_sm : info.screen_ctas_per_sm);
+        const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+        idx_cp_kernel<<<grid, T, cpi_smem<T>(), stream>>>(ld.verts, ld.idx, a.n, body);
     });
 }
 
@@ -2107,10 +2186,13 @@ void launch_wtma(const SoaLoader& ld, const DeviceInfo& info, const P1Args& a, c
 }
 
 void launch_cp(const SoaLoader& ld, const DeviceInfo& info, const P1Args& a, cudaStream_t stream) {
-    const int64_t tiles = (a.n + CP_THREADS - 1) / CP_THREADS;
-    const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
-    const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-    with_pass1_body(a, [&](auto body) { soa_cp_kernel<<<grid, CP_THREADS, CP_SMEM, stream>>>(ld.coords, a.n, body); });
+    with_pass1_body(a, [&](auto body) {
+        constexpr int T = decltype(body)::THREADS;
+        const int64_t tiles = (a.n + T - 1) / T;
+        const int64_t cap = (int64_t)info.sms * (T == CP_THREADS ? info.p1_ctas_per_sm : info.screen_ctas_per_sm);
+        const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+        soa_cp_kernel<<<grid, T, cp_smem<T>(), stream>>>(ld.coords, a.n, body);
+    });
 }
 
 // SoA: the selected variant (warp-TMA needs a 16-B aligned coordinate array
