@@ -71,13 +71,7 @@ constexpr int K4_MINB = HEXVAL_K4_MINB;
 #else
 #define HV_K4_BOUNDS __launch_bounds__(K4_THREADS, K4_MINB)
 #endif
-// The subdivision kernel with its node's xi split parked in tensor memory
-// (HEXVAL_K4_TMEM): 3 blocks of 4 warps per SM (<= 168 registers)
-#ifdef HEXVAL_K4_TMEM
-#define HV_SUBDIV_BOUNDS __launch_bounds__(K4_THREADS, 3)
-#else
-#define HV_SUBDIV_BOUNDS HV_K4_BOUNDS
-#endif
+
 
 // flags placeholders written by pass 1 for hexes that later kernels finish
 constexpr uint8_t PENDING_EXACT = 0xFF;
@@ -940,6 +934,11 @@ __device__ __forceinline__ void ld_v4(const double* p, double& a, double& b, dou
 __device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
     asm volatile(HV_ST_V4 " [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
+// the same store predicated on `on` (no divergent branch around a lane's push)
+__device__ __forceinline__ void st_v4_if(bool on, double* p, double a, double b, double c, double d) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q " HV_ST_V4 " [%0], {%1,%2,%3,%4};\n\t}"
+                 ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d), "r"((unsigned)on) : "memory");
+}
 
 // A node on the stack: 7 x 32-byte vectors per slot, coalesced over the warp's
 // consecutive slots; value 27 is the meta word (low half: owner = batch slot of
@@ -954,6 +953,24 @@ __device__ __forceinline__ unsigned long long stack_load(const double* sc, int s
     }
     return (unsigned long long)__double_as_longlong(m);
 }
+__device__ __forceinline__ void stack_store_if(bool on, double* sc, int slot, const double* C, unsigned long long meta) {
+    // one predicate for the node's 7 vector stores (offsets: K4_CAP * 32 bytes per vector)
+    double* dst = sc + (size_t)slot * 4;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %29, 0;\n\t"
+                 "@q " HV_ST_V4 " [%0], {%1,%2,%3,%4};\n\t"
+                 "@q " HV_ST_V4 " [%0+155648], {%5,%6,%7,%8};\n\t"
+                 "@q " HV_ST_V4 " [%0+311296], {%9,%10,%11,%12};\n\t"
+                 "@q " HV_ST_V4 " [%0+466944], {%13,%14,%15,%16};\n\t"
+                 "@q " HV_ST_V4 " [%0+622592], {%17,%18,%19,%20};\n\t"
+                 "@q " HV_ST_V4 " [%0+778240], {%21,%22,%23,%24};\n\t"
+                 "@q " HV_ST_V4 " [%0+933888], {%25,%26,%27,%28};\n\t}"
+                 ::"l"(dst), "d"(C[0]), "d"(C[1]), "d"(C[2]), "d"(C[3]), "d"(C[4]), "d"(C[5]), "d"(C[6]), "d"(C[7]),
+                 "d"(C[8]), "d"(C[9]), "d"(C[10]), "d"(C[11]), "d"(C[12]), "d"(C[13]), "d"(C[14]), "d"(C[15]),
+                 "d"(C[16]), "d"(C[17]), "d"(C[18]), "d"(C[19]), "d"(C[20]), "d"(C[21]), "d"(C[22]), "d"(C[23]),
+                 "d"(C[24]), "d"(C[25]), "d"(C[26]), "d"(__longlong_as_double((long long)meta)), "r"((unsigned)on)
+                 : "memory");
+}
+static_assert(K4_CAP * 32 == 155648, "stack_store_if's vector offsets");
 __device__ __forceinline__ void stack_store(double* sc, int slot, const double* C, unsigned long long meta) {
 #pragma unroll
     for (int q = 0; q < 7; ++q) {
@@ -1099,148 +1116,9 @@ __device__ __forceinline__ void split_quarter_s(const double* G1, int hx, int hy
 }
 
 
-// ---- tensor memory as a per-thread scratchpad (HEXVAL_K4_TMEM) -----------
-// In the 32x32b shape thread t of warp w reads and writes TMEM lane
-// 32 (w mod 4) + t: a lane-private array of 32-bit columns.  K4 parks the
-// node's xi split there -- the five xi positions a as 9-value columns
-// g[j + 3k] -- and reads one column back per eta split, so the split's live
-// set drops from 45 + 45 to 9 + 45 values and 3 blocks of 4 warps fit an SM.
-// Nodes on the stack are i-major in this build (NI), so that the two xi
-// positions a = 0, 4 of a popped node are contiguous runs of its vectors.
-// Columns (32-bit): a0 -> 0, a4 -> 18, a1 (s01) -> 36, a2 (sm) -> 54,
-// a3 (s12) -> 72; each eta split's second half (hy = 1) is parked in a column
-// that is dead by then (hx = 0: 0, 36, 90; hx = 1: 54, 72, 18).
-#ifdef HEXVAL_K4_TMEM
-__host__ __device__ constexpr int NI(int i, int j, int k) { return 9 * i + j + 3 * k; }
-#else
+// Node layout on the stack: coefficient (i, j, k) of a node at NI(i, j, k) (the
+// layout of the root coefficients, i + 3j + 9k).
 __host__ __device__ constexpr int NI(int i, int j, int k) { return i + 3 * j + 9 * k; }
-#endif
-struct TmemSplit {
-    uint32_t taddr;          // this warp's lane quarter, column 0 of the block's allocation
-    __device__ __forceinline__ static constexpr int COL(int a) { return a == 0 ? 0 : (a == 4 ? 18 : 18 + 18 * a); }
-    __device__ __forceinline__ static constexpr int PARK(int hx, int c) {
-        return hx == 0 ? (c == 0 ? 0 : (c == 1 ? 36 : 90)) : (c == 0 ? 54 : (c == 1 ? 72 : 18));
-    }
-    // one 2-column store per double: a double is already an aligned register pair, so
-    // no register moves are needed to gather the 9 values into a 16-register block
-    __device__ __forceinline__ void put9(int col, const double* v) const {
-#pragma unroll
-        for (int q = 0; q < 9; ++q)
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr + col + 2 * q),
-                         "r"(__double2loint(v[q])), "r"(__double2hiint(v[q])) : "memory");
-    }
-    // 2^n doubles (n = 0, 1, 2) from consecutive registers (e.g. one 256-bit stack vector)
-    template <int N>
-    __device__ __forceinline__ void putN(int col, const double* v) const {
-        if (N == 4)
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr + col),
-                         "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])),
-                         "r"(__double2hiint(v[1])), "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])),
-                         "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])) : "memory");
-        else if (N == 2)
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr + col),
-                         "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])),
-                         "r"(__double2hiint(v[1])) : "memory");
-        else
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr + col),
-                         "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])) : "memory");
-    }
-    __device__ __forceinline__ void get9(int col, double* v) const {
-        uint32_t w[18];
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
-                       "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]),
-                       "=r"(w[15])
-                     : "r"(taddr + col) : "memory");
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(w[16]), "=r"(w[17])
-                     : "r"(taddr + col + 16) : "memory");
-        // the wait names the destination registers so that no use is scheduled above it
-        asm volatile("tcgen05.wait::ld.sync.aligned;"
-                     : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]),
-                       "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]), "+r"(w[12]), "+r"(w[13]), "+r"(w[14]),
-                       "+r"(w[15]), "+r"(w[16]), "+r"(w[17])
-                     :: "memory");
-#pragma unroll
-        for (int q = 0; q < 9; ++q) v[q] = __hiloint2double((int)w[2 * q + 1], (int)w[2 * q]);
-    }
-    __device__ __forceinline__ static void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-};
-
-// xi split of an i-major node into TMEM: the columns a = 0, 4 are the node's
-// own xi = 0, 2 slabs, a = 1, 2, 3 the scaled de Casteljau values of the 9 lines
-__device__ __forceinline__ void split_xi_tm(const double* P, const SplitScale& sc, const TmemSplit& tm) {
-    double s01[9], sm[9], s12[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) line_split_s(P[q], P[9 + q], P[18 + q], sc.r01[0], sc.r21[0], s01[q], sm[q], s12[q]);
-    // the xi = 0, 2 slabs straight from the popped node's 256-bit vectors (P[0..3], P[4..7], ...)
-    // (a 256-bit load fills two 4-register groups: one 4-column store per group)
-#pragma unroll
-    for (int q = 0; q < 8; q += 2) tm.putN<2>(TmemSplit::COL(0) + 2 * q, P + q);
-    tm.putN<1>(TmemSplit::COL(0) + 16, P + 8);
-#pragma unroll
-    for (int q = 0; q < 8; q += 2) tm.putN<2>(TmemSplit::COL(4) + 2 * q, P + 18 + q);
-    tm.putN<1>(TmemSplit::COL(4) + 16, P + 26);
-    tm.put9(TmemSplit::COL(1), s01);
-    tm.put9(TmemSplit::COL(2), sm);
-    tm.put9(TmemSplit::COL(3), s12);
-    TmemSplit::wait_st();
-}
-
-// eta split of column c of xi half hx: half hy = 0 goes into the quarter Z (zeta
-// split, layout of split_quarter_s), half hy = 1 is parked in TMEM
-__device__ __forceinline__ void eta_zeta_tm(const TmemSplit& tm, int hx, int c, const SplitScale& sc, double* Z) {
-    double g[9];
-    tm.get9(TmemSplit::COL(2 * hx + c), g);
-    double B0[9], B1[9];                                 // B[u + 3k]
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        double s01, sm, s12;
-        line_split_s(g[3 * k], g[1 + 3 * k], g[2 + 3 * k], sc.r01[1], sc.r21[1], s01, sm, s12);
-        B0[3 * k] = g[3 * k]; B0[1 + 3 * k] = s01; B0[2 + 3 * k] = sm;
-        B1[3 * k] = sm; B1[1 + 3 * k] = s12; B1[2 + 3 * k] = g[2 + 3 * k];
-    }
-    tm.put9(TmemSplit::PARK(hx, c), B1);
-#pragma unroll
-    for (int u = 0; u < 3; ++u) {
-        double s01, sm, s12;
-        line_split_s(B0[u], B0[u + 3], B0[u + 6], sc.r01[2], sc.r21[2], s01, sm, s12);
-        double* z = Z + c + 3 * u;
-        z[0] = B0[u]; z[9] = s01; z[18] = sm; z[27] = s12; z[36] = B0[u + 6];
-    }
-}
-// the parked hy = 1 half of column c: zeta split into Z
-__device__ __forceinline__ void zeta_parked_tm(const TmemSplit& tm, int hx, int c, const SplitScale& sc, double* Z) {
-    double B1[9];
-    tm.get9(TmemSplit::PARK(hx, c), B1);
-#pragma unroll
-    for (int u = 0; u < 3; ++u) {
-        double s01, sm, s12;
-        line_split_s(B1[u], B1[u + 3], B1[u + 6], sc.r01[2], sc.r21[2], s01, sm, s12);
-        double* z = Z + c + 3 * u;
-        z[0] = B1[u]; z[9] = s01; z[18] = sm; z[27] = s12; z[36] = B1[u + 6];
-    }
-}
-
-struct TmemBlock {           // the block's TMEM allocation (one warp allocates and frees)
-    static constexpr int COLS = 128;
-    __device__ __forceinline__ static uint32_t alloc(uint32_t* slot) {
-        if (threadIdx.x < 32) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
-                         "n"(COLS));
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        return *((volatile uint32_t*)slot);
-    }
-    __device__ __forceinline__ static void free(uint32_t base) {
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(COLS));
-    }
-};
 
 struct K4Warp {
     unsigned status[32];    // per batch slot: bit 0 INVALID found, bit 1 depth cap reached
@@ -1342,7 +1220,7 @@ struct CoeffRoot {
 };
 
 template <class R, bool STATS>
-__global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
+__global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, Ctl* ctl,
                                                             const uint32_t* __restrict__ qsub,
                                                             const uint32_t* __restrict__ qexact, WarpStacks ws,
                                                             hexval_stats* stats) {
@@ -1351,12 +1229,6 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
     K4Warp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
     double* const sc = ws.coef + gw * 28 * K4_CAP;
-#ifdef HEXVAL_K4_TMEM
-    static_assert(K4_THREADS == 128, "one warp per TMEM lane quarter");
-    __shared__ uint32_t tmem_slot;
-    const uint32_t tmem_base = TmemBlock::alloc(&tmem_slot);
-    const TmemSplit tm{tmem_base + ((uint32_t)(32 * (threadIdx.x >> 5)) << 16)};
-#endif
     const unsigned total = *((volatile unsigned*)&ctl->n_sub);
     const unsigned n_exact = *((volatile unsigned*)&ctl->n_exact);
     bool ex_left = n_exact > 0;                          // warp-uniform: the exact queue may hold items
@@ -1454,12 +1326,8 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
         // ---- split every active node into its 8 children --------------------
         SplitScale ss;
         ss.unpack(pat);
-#ifdef HEXVAL_K4_TMEM
-        split_xi_tm(P, ss, tm);
-#else
         double G1[45];
         split_xi_s(P, ss, G1);
-#endif
         if (d > 0 && act) act = (ld_shared_u32(&W.status[owner]) & 1u) == 0;   // hex already INVALID: drop the node
         if (STATS) {
             const unsigned actmask = __ballot_sync(0xffffffffu, act);
@@ -1505,9 +1373,17 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
 #pragma unroll
                     for (int hz = 0; hz < 2; ++hz) {
                         const unsigned bm = hz ? b1 : b0;
+#ifndef HEXVAL_K4_BRANCHED_PUSH
+                        if (bm) {                                  // warp-uniform; the lanes' stores are predicated
+                            const bool mine = (bm >> lane) & 1u;
+                            const int slot = top + pushed + (hz ? c0 : 0) + __popc(bm & lt_mask);
+                            HV_CHECK(!mine || (slot >= 0 && slot < K4_CAP && owner >= 0 && owner < 32));
+#else
                         if (bm & (1u << lane)) {
+                            const bool mine = true;
                             const int slot = top + pushed + (hz ? c0 : 0) + __popc(bm & lt_mask);
                             HV_CHECK(slot >= 0 && slot < K4_CAP && owner >= 0 && owner < 32);
+#endif
                             double C[27];
 #pragma unroll
                             for (int v = 0; v < 3; ++v)
@@ -1515,28 +1391,14 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
                                 for (int u = 0; u < 3; ++u)
 #pragma unroll
                                     for (int a = 0; a < 3; ++a) C[NI(a, u, v)] = Z[a + 3 * u + 9 * (2 * hz + v)];
-                            stack_store(sc, slot, C,
-                                        (unsigned long long)(unsigned)owner |
-                                            ((unsigned long long)ss.child(hx, hy, hz) << 32));
-
+                            stack_store_if(mine, sc, slot, C,
+                                           (unsigned long long)(unsigned)owner |
+                                               ((unsigned long long)ss.child(hx, hy, hz) << 32));
                         }
                     }
                     pushed += c0 + __popc(b1);
                 }
         };
-#ifdef HEXVAL_K4_TMEM
-#pragma unroll
-        for (int hx = 0; hx < 2; ++hx) {
-            double Z[45];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) eta_zeta_tm(tm, hx, c, ss, Z);
-            quarter(hx, 0, Z);
-            TmemSplit::wait_st();
-#pragma unroll
-            for (int c = 0; c < 3; ++c) zeta_parked_tm(tm, hx, c, ss, Z);
-            quarter(hx, 1, Z);
-        }
-#else
 #pragma unroll
         for (int hx = 0; hx < 2; ++hx)
 #pragma unroll
@@ -1545,7 +1407,6 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
                 split_quarter_s(G1, hx, hy, ss, Z);
                 quarter(hx, hy, Z);
             }
-#endif
         if (inval) atomicOr(&W.status[owner], 1u);
         if (capped) atomicOr(&W.status[owner], 2u);
         top += pushed;
@@ -1581,9 +1442,6 @@ __global__ void HV_SUBDIV_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ fla
             }
         }
     }
-#ifdef HEXVAL_K4_TMEM
-    TmemBlock::free(tmem_base);
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -2090,11 +1948,6 @@ const DeviceInfo& device_info(int dev) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, subdiv_kernel<CoordRoot<SoaLoader>, false>, K4_THREADS,
                                                       0);
         d.k4_blocks_per_sm = occ > 0 ? occ : 1;
-#ifdef HEXVAL_K4_TMEM
-        // the occupancy calculator assumes a tcgen05.alloc kernel may hold the whole
-        // 512-column TMEM and reports 1 block/SM; 3 blocks x 128 columns fit
-        d.k4_blocks_per_sm = 3;
-#endif
         const int want = pass1_variant_from_env();
         const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup(&d.screen_ctas_per_sm) : 0);
         d.p1_variant = ctas > 0 ? want : P1_LDG;
