@@ -619,13 +619,16 @@ __global__ void __launch_bounds__(WT_THREADS, 2)
 #endif
 constexpr int CP_THREADS = HEXVAL_CP_THREADS;        // A/B builds: 128 x 4 or 256 x 2 CTAs/SM (16 warps/SM)
 constexpr int CP_MINB = 512 / CP_THREADS;
-constexpr size_t CP_SMEM = (size_t)2 * 24 * CP_THREADS * sizeof(double);   // 96 KB: two tiles
+constexpr size_t CP_SMEM = (size_t)2 * 24 * CP_THREADS * sizeof(double);   // 96 KB: two tiles (indexed kernel)
 // The fused validity + screening pass (QUAL bodies) carries more live state per hex: it runs
 // with its own block size (A/B knob; 384 x 1 = 12 warps/SM at <= 168 registers).
 #ifndef HEXVAL_SCREEN_THREADS
 #define HEXVAL_SCREEN_THREADS 384
 #endif
-template <int T> constexpr size_t cp_smem() { return (size_t)2 * 24 * T * sizeof(double); }
+#ifndef HEXVAL_CP_STAGES
+#define HEXVAL_CP_STAGES 2
+#endif
+template <int T, int S = 2> constexpr size_t cp_smem() { return (size_t)S * 24 * T * sizeof(double); }
 template <int T> constexpr int cp_minb() { return T >= 512 ? 1 : 512 / T; }
 
 __device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, uint64_t policy) {
@@ -634,6 +637,8 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, uint6
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int T>
 __device__ __forceinline__ void cp_issue_hex(const double* __restrict__ coords, int64_t n, int64_t i, uint32_t dst) {
@@ -652,6 +657,7 @@ template <bool COEFFS, bool STATS, bool QUAL = false>
 struct Pass1Body {                                           // K1/K2: S1-S8 + K3 (+ NEXT-2 outputs)
     static constexpr int THREADS = QUAL ? HEXVAL_SCREEN_THREADS : CP_THREADS;
     static constexpr int MINB = cp_minb<THREADS>();
+    static constexpr int STAGES = QUAL ? 2 : HEXVAL_CP_STAGES;   // SoA pipeline depth (soa_cp_kernel)
     int64_t n;
     uint8_t* flags;
     double* coeffs;
@@ -691,13 +697,13 @@ __global__ void __launch_bounds__(Body::THREADS, Body::MINB)
     const tile_t tiles = (tile_t)((n + CP_THREADS - 1) / CP_THREADS);
     const tile_t G = (tile_t)gridDim.x;
     const uint32_t s0 = smem_u32(cp_buf + tid);
-    const uint32_t s1 = s0 + 24 * CP_THREADS * 8;
+    constexpr int S = Body::STAGES;                          // tiles in flight + 1
+    constexpr uint32_t SB = 24 * CP_THREADS * 8;             // bytes per stage
     tile_t t = blockIdx.x;
-    cp_issue_hex<CP_THREADS>(coords, n, (int64_t)t * CP_THREADS + tid, s0);
-    cp_issue_hex<CP_THREADS>(coords, n, (int64_t)(t + G) * CP_THREADS + tid, s1);
-    for (int k = 0; t < tiles; t += G, ++k) {
-        const int b = k & 1;
-        cp_async_wait1();                                    // tile k has landed (tile k+1 may be in flight)
+#pragma unroll
+    for (int j = 0; j < S; ++j) cp_issue_hex<CP_THREADS>(coords, n, (int64_t)(t + j * G) * CP_THREADS + tid, s0 + j * SB);
+    for (int b = 0; t < tiles; t += G, b = (b + 1 == S ? 0 : b + 1)) {
+        cp_async_wait<S - 1>();                              // tile k has landed (tiles k+1.. may be in flight)
         const int64_t i = (int64_t)t * CP_THREADS + tid;
         int st = -1;
         if (i < n) {
@@ -707,8 +713,8 @@ __global__ void __launch_bounds__(Body::THREADS, Body::MINB)
             for (int p = 0; p < 24; ++p) X[p] = src[p * CP_THREADS];
             st = body.hex(SoaLoader{coords, n}, X, i);
         }
-        // refill this buffer with tile k+2 (X was consumed above: program order)
-        cp_issue_hex<CP_THREADS>(coords, n, (int64_t)(t + 2 * G) * CP_THREADS + tid, b ? s1 : s0);
+        // refill this buffer with tile k+S (X was consumed above: program order)
+        cp_issue_hex<CP_THREADS>(coords, n, (int64_t)(t + S * G) * CP_THREADS + tid, s0 + b * SB);
         body.epilogue(st, i);
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -938,6 +944,24 @@ __device__ __forceinline__ void st_v4(double* p, double a, double b, double c, d
 __device__ __forceinline__ void st_v4_if(bool on, double* p, double a, double b, double c, double d) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q " HV_ST_V4 " [%0], {%1,%2,%3,%4};\n\t}"
                  ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d), "r"((unsigned)on) : "memory");
+}
+
+// Popped stack lines are dead; HEXVAL_K4_DISCARD invalidates them in L2 instead of
+// letting them be written back: lines wholly inside the popped slots [lo, lo + k)
+// (4 slots per 128-byte line; the line of slot lo + k - 1 extends only into free
+// slots above the top).  Measured on config 4 (K4_EXPERIMENTS.md): HBM writes
+// 195 -> 27.7 GB per call, but the kernel 249 -> 265 ms (the CCTL per line costs more
+// than the write-backs, which HBM absorbs at ~0.8 TB/s): off by default.
+__device__ __forceinline__ void discard_popped(const double* sc, int lo, int k, int lane) {
+#ifdef HEXVAL_K4_DISCARD
+    const int f = (lo + 3) >> 2, nl = ((lo + k - 1) >> 2) - f + 1;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int idx = lane + 32 * r, q = idx >> 3, j = idx & 7;
+        if (q < 7 && j < nl)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(sc + ((size_t)q * K4_CAP + 4 * (f + j)) * 4) : "memory");
+    }
+#endif
 }
 
 // A node on the stack: 7 x 32-byte vectors per slot, coalesced over the warp's
@@ -1240,7 +1264,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
     for (;;) {
         double P[27];
         bool act;
-        int owner = lane, d;
+        int owner = lane, d, popped;
         unsigned pat = ROOT_PATTERN;                     // scale pattern of the node (see SplitScale)
         if (top == 0) {
             // batch done: write its verdicts (precedence INVALID > UNDETERMINED > VALID, reading G4)
@@ -1322,12 +1346,14 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             }
             top -= k;
             lc.tcnt -= k;
+            popped = k;
         }
         // ---- split every active node into its 8 children --------------------
         SplitScale ss;
         ss.unpack(pat);
         double G1[45];
         split_xi_s(P, ss, G1);
+        discard_popped(sc, top, popped, lane);   // P is consumed: the popped lines are dead
         if (d > 0 && act) act = (ld_shared_u32(&W.status[owner]) & 1u) == 0;   // hex already INVALID: drop the node
         if (STATS) {
             const unsigned actmask = __ballot_sync(0xffffffffu, act);
@@ -1899,7 +1925,7 @@ int wtma_setup() {
 }
 
 template <class Body>
-bool cp_attr(size_t smem_soa = cp_smem<Body::THREADS>(), size_t smem_idx = cpi_smem<Body::THREADS>()) {
+bool cp_attr(size_t smem_soa = cp_smem<Body::THREADS, Body::STAGES>(), size_t smem_idx = cpi_smem<Body::THREADS>()) {
     return cudaFuncSetAttribute((const void*)soa_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem_soa) == cudaSuccess &&
            cudaFuncSetAttribute((const void*)idx_cp_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1907,8 +1933,8 @@ bool cp_attr(size_t smem_soa = cp_smem<Body::THREADS>(), size_t smem_idx = cpi_s
 }
 
 int cp_setup(int* screen_ctas) {
-    const bool ok = cp_attr<Pass1Body<false, false>>(CP_SMEM, CPI_SMEM) && cp_attr<Pass1Body<false, true>>(CP_SMEM, CPI_SMEM) &&
-                    cp_attr<Pass1Body<true, false>>(CP_SMEM, CPI_SMEM) && cp_attr<Pass1Body<true, true>>(CP_SMEM, CPI_SMEM) &&
+    const bool ok = cp_attr<Pass1Body<false, false>>() && cp_attr<Pass1Body<false, true>>() &&
+                    cp_attr<Pass1Body<true, false>>() && cp_attr<Pass1Body<true, true>>() &&
                     cp_attr<Pass1Body<false, false, true>>() && cp_attr<Pass1Body<false, true, true>>();
     if (!ok) {
         cudaGetLastError();
@@ -1917,9 +1943,9 @@ int cp_setup(int* screen_ctas) {
     int occ = 0, socc = 0;
     using SB = Pass1Body<false, false, true>;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, soa_cp_kernel<Pass1Body<false, false>>, CP_THREADS,
-                                                      CP_SMEM) != cudaSuccess ||
+                                                      cp_smem<CP_THREADS, HEXVAL_CP_STAGES>()) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&socc, soa_cp_kernel<SB>, SB::THREADS,
-                                                      cp_smem<SB::THREADS>()) != cudaSuccess) {
+                                                      cp_smem<SB::THREADS, SB::STAGES>()) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -2044,7 +2070,7 @@ void launch_cp(const SoaLoader& ld, const DeviceInfo& info, const P1Args& a, cud
         const int64_t tiles = (a.n + T - 1) / T;
         const int64_t cap = (int64_t)info.sms * (T == CP_THREADS ? info.p1_ctas_per_sm : info.screen_ctas_per_sm);
         const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-        soa_cp_kernel<<<grid, T, cp_smem<T>(), stream>>>(ld.coords, a.n, body);
+        soa_cp_kernel<<<grid, T, cp_smem<T, decltype(body)::STAGES>(), stream>>>(ld.coords, a.n, body);
     });
 }
 
