@@ -1494,7 +1494,6 @@ struct BWarp {
     double tol[32];
     unsigned capped[32];
     uint32_t hex[32];
-    int cnt[MAX_DEPTH + 1];
 };
 
 // Root phase of NEXT-1: one hex per thread; a hex whose root coefficients
@@ -1558,8 +1557,7 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
     double* const sc = ws.coef + gw * 28 * K4_CAP;
     const unsigned lt_mask = (1u << lane) - 1u;
-    if (lane <= MAX_DEPTH) W.cnt[lane] = 0;
-    __syncwarp();
+    LevelCounts lc;
     int top = 0, D = 0, nb = 0;
     unsigned long long nodes = 0;
     const unsigned total = *((volatile unsigned*)&ctlq[0]);
@@ -1600,7 +1598,7 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
                 act = true;                                  // queued: the root is split
             }
         } else {
-            const int k = min(32, W.cnt[D]);
+            const int k = min(32, lc.tcnt);
             HV_CHECK(D > 0 && D < MAX_DEPTH && k > 0 && k <= top);
             d = D;
             if (lane < k) {
@@ -1615,8 +1613,7 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
                 else act = true;
             }
             top -= k;
-            __syncwarp();
-            if (lane == 0) W.cnt[D] -= k;
+            lc.tcnt -= k;
         }
         __syncwarp();
         nodes += __popc(__ballot_sync(0xffffffffu, act));
@@ -1681,13 +1678,7 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
                 }
             }
         top += pushed;
-        __syncwarp();
-        if (pushed) {
-            if (lane == 0) W.cnt[d + 1] += pushed;
-            D = d + 1;
-        } else {
-            while (D > 0 && W.cnt[D] == 0) --D;
-        }
+        lc.after_step(lane, d, pushed, D);
         __syncwarp();
     }
     if (nodes_out && lane == 0 && nodes) atomicAdd(nodes_out, nodes);
