@@ -618,8 +618,6 @@ __global__ void __launch_bounds__(WT_THREADS, 2)
 #define HEXVAL_CP_THREADS 256
 #endif
 constexpr int CP_THREADS = HEXVAL_CP_THREADS;        // A/B builds: 128 x 4 or 256 x 2 CTAs/SM (16 warps/SM)
-constexpr int CP_MINB = 512 / CP_THREADS;
-constexpr size_t CP_SMEM = (size_t)2 * 24 * CP_THREADS * sizeof(double);   // 96 KB: two tiles (indexed kernel)
 // The fused validity + screening pass (QUAL bodies) carries more live state per hex: it runs
 // with its own block size (A/B knob; 384 x 1 = 12 warps/SM at <= 168 registers).
 #ifndef HEXVAL_SCREEN_THREADS
@@ -702,7 +700,11 @@ __global__ void __launch_bounds__(Body::THREADS, Body::MINB)
     tile_t t = blockIdx.x;
 #pragma unroll
     for (int j = 0; j < S; ++j) cp_issue_hex<CP_THREADS>(coords, n, (int64_t)(t + j * G) * CP_THREADS + tid, s0 + j * SB);
-    for (int b = 0; t < tiles; t += G, b = (b + 1 == S ? 0 : b + 1)) {
+    // buffer index: k & 1 for the default double buffer (the generic counter below costs
+    // 1.3% on config 1: 333.4 vs 328.9 us, 4 interleaved reps, profiles/r02/PASS1_EXPERIMENTS.md)
+    int b = 0;
+    for (int k = 0; t < tiles; t += G, ++k) {
+        if (S == 2) b = k & 1;
         cp_async_wait<S - 1>();                              // tile k has landed (tiles k+1.. may be in flight)
         const int64_t i = (int64_t)t * CP_THREADS + tid;
         int st = -1;
@@ -714,8 +716,9 @@ __global__ void __launch_bounds__(Body::THREADS, Body::MINB)
             st = body.hex(SoaLoader{coords, n}, X, i);
         }
         // refill this buffer with tile k+S (X was consumed above: program order)
-        cp_issue_hex<CP_THREADS>(coords, n, (int64_t)(t + S * G) * CP_THREADS + tid, s0 + b * SB);
+        cp_issue_hex<CP_THREADS>(coords, n, (int64_t)(t + S * G) * CP_THREADS + tid, S == 2 ? (b ? s0 + SB : s0) : s0 + b * SB);
         body.epilogue(st, i);
+        if (S != 2) b = b + 1 == S ? 0 : b + 1;
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     body.finish();
@@ -728,8 +731,7 @@ __global__ void __launch_bounds__(Body::THREADS, Body::MINB)
 // connectivity row of tile k+2 (two 16-byte async copies into shared memory);
 // after computing, the thread reads that row from shared memory and issues the
 // gathers of tile k+2.  No register holds prefetched data across the compute.
-constexpr size_t CPI_SMEM = CP_SMEM + (size_t)2 * CP_THREADS * 32 + (size_t)2 * CP_THREADS;   // + two idx tiles, two dup-flag tiles
-template <int T> constexpr size_t cpi_smem() { return cp_smem<T>() + (size_t)2 * T * 32 + (size_t)2 * T; }
+template <int T> constexpr size_t cpi_smem() { return cp_smem<T>() + (size_t)2 * T * 32 + (size_t)2 * T; }   // + two idx tiles, two dup-flag tiles
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
@@ -940,11 +942,6 @@ __device__ __forceinline__ void ld_v4(const double* p, double& a, double& b, dou
 __device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
     asm volatile(HV_ST_V4 " [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
-// the same store predicated on `on` (no divergent branch around a lane's push)
-__device__ __forceinline__ void st_v4_if(bool on, double* p, double a, double b, double c, double d) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t@q " HV_ST_V4 " [%0], {%1,%2,%3,%4};\n\t}"
-                 ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d), "r"((unsigned)on) : "memory");
-}
 
 // Popped stack lines are dead; HEXVAL_K4_DISCARD invalidates them in L2 instead of
 // letting them be written back: lines wholly inside the popped slots [lo, lo + k)
@@ -1140,10 +1137,6 @@ __device__ __forceinline__ void split_quarter_s(const double* G1, int hx, int hy
 }
 
 
-// Node layout on the stack: coefficient (i, j, k) of a node at NI(i, j, k) (the
-// layout of the root coefficients, i + 3j + 9k).
-__host__ __device__ constexpr int NI(int i, int j, int k) { return i + 3 * j + 9 * k; }
-
 struct K4Warp {
     unsigned status[32];    // per batch slot: bit 0 INVALID found, bit 1 depth cap reached
     uint32_t hex[32];       // hex id of each batch slot
@@ -1316,15 +1309,9 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             // stack as level 0, so that every step takes its nodes from one place
             if (lane < nb) {
                 W.status[lane] = 0;
-                double R[27], Rn[27];
-                root(W.hex[lane], R);
-#pragma unroll
-                for (int k = 0; k < 3; ++k)
-#pragma unroll
-                    for (int j = 0; j < 3; ++j)
-#pragma unroll
-                        for (int i = 0; i < 3; ++i) Rn[NI(i, j, k)] = R[i + 3 * j + 9 * k];   // the stack's node layout
-                stack_store(sc, lane, Rn, (unsigned long long)(unsigned)lane | ((unsigned long long)ROOT_PATTERN << 32));
+                double rc[27];
+                root(W.hex[lane], rc);
+                stack_store(sc, lane, rc, (unsigned long long)(unsigned)lane | ((unsigned long long)ROOT_PATTERN << 32));
             }
             top = nb;
             lc.tcnt = nb;
@@ -1416,7 +1403,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
 #pragma unroll
                                 for (int u = 0; u < 3; ++u)
 #pragma unroll
-                                    for (int a = 0; a < 3; ++a) C[NI(a, u, v)] = Z[a + 3 * u + 9 * (2 * hz + v)];
+                                    for (int a = 0; a < 3; ++a) C[a + 3 * u + 9 * v] = Z[a + 3 * u + 9 * (2 * hz + v)];
                             stack_store_if(mine, sc, slot, C,
                                            (unsigned long long)(unsigned)owner |
                                                ((unsigned long long)ss.child(hx, hy, hz) << 32));

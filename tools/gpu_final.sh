@@ -30,4 +30,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:idx_
 CMD4="python bench.py --config 4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-cupti"
 timeout 600 $CMD4 > $O/plain4.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:subdiv -s 1 -c 1 -o $O/subdiv_c4 $CMD4 > $O/ncu_f4.log 2>&1
-echo done
+echo done1
+CMDS="python bench.py --op screen --config 1 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-cupti --no-secondary"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:soa_cp_kernel -s 4 -c 1 -o $O/screen_c1 $CMDS > $O/ncu_fs.log 2>&1
+echo done2
