@@ -1706,8 +1706,21 @@ __global__ void __launch_bounds__(SEL_THREADS) select_count_kernel(const uint8_t
     const int64_t i0 = (int64_t)blockIdx.x * SEL_TILE + (int64_t)threadIdx.x * 16;
     const unsigned m = valid_mask16(flags, n, i0);
     if (group_counts && m) {
+        if (i0 + 16 <= n && ((((uintptr_t)(group + i0)) & 15) == 0)) {
+            // the 16 group ids in four 16-B loads, then one reduction per VALID candidate
+            int g[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int4 v = __ldcs(reinterpret_cast<const int4*>(group + i0) + q);
+                g[4 * q] = v.x; g[4 * q + 1] = v.y; g[4 * q + 2] = v.z; g[4 * q + 3] = v.w;
+            }
+#pragma unroll
+            for (int b = 0; b < 16; ++b)
+                if ((m >> b) & 1u) atomicAdd(&group_counts[g[b]], 1);
+        } else {
 #pragma unroll 1
-        for (unsigned r = m; r; r &= r - 1) atomicAdd(&group_counts[__ldg(group + i0 + __ffs(r) - 1)], 1);
+            for (unsigned r = m; r; r &= r - 1) atomicAdd(&group_counts[__ldg(group + i0 + __ffs(r) - 1)], 1);
+        }
     }
     unsigned c = __popc(m);
 #pragma unroll
@@ -1764,6 +1777,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_write_kernel(const uint8_t
                                                                      const unsigned* __restrict__ tile_offsets,
                                                                      int32_t* __restrict__ ids) {
     __shared__ unsigned s_w[SEL_THREADS / 32];
+    __shared__ int32_t s_ids[SEL_THREADS / 32][32 * 16];              // a warp's ids in order, then copied out
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t i0 = (int64_t)blockIdx.x * SEL_TILE + (int64_t)threadIdx.x * 16;
     const unsigned m = valid_mask16(flags, n, i0);
@@ -1779,11 +1793,19 @@ __global__ void __launch_bounds__(SEL_THREADS) select_write_kernel(const uint8_t
     unsigned before = 0;
 #pragma unroll
     for (int q = 0; q < SEL_THREADS / 32; ++q) before += q < w ? s_w[q] : 0u;
-    unsigned pos = tile_offsets[blockIdx.x] + before + x - c;
+    // each lane's ids go to their ordered places in the warp's staging row (shared
+    // memory takes the scattered writes), then the warp writes the row out coalesced
+    int32_t* const row = s_ids[w];
+    unsigned p = x - c;
 #pragma unroll 1
-    for (unsigned r = m; r; r &= r - 1) {
-        HV_CHECK((int64_t)pos < n);
-        ids[pos++] = (int32_t)(i0 + __ffs(r) - 1);
+    for (unsigned r = m; r; r &= r - 1) row[p++] = (int32_t)(i0 + __ffs(r) - 1);
+    __syncwarp();
+    const unsigned total = __shfl_sync(0xffffffffu, x, 31);
+    const unsigned base = tile_offsets[blockIdx.x] + before;
+#pragma unroll 1
+    for (unsigned q = lane; q < total; q += 32) {
+        HV_CHECK((int64_t)(base + q) < n);
+        ids[base + q] = row[q];
     }
 }
 
