@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(Body::THREADS, Body::MINB)
 // connectivity row of tile k+2 (two 16-byte async copies into shared memory);
 // after computing, the thread reads that row from shared memory and issues the
 // gathers of tile k+2.  No register holds prefetched data across the compute.
-template <int T> constexpr size_t cpi_smem() { return cp_smem<T>() + (size_t)2 * T * 32 + (size_t)2 * T; }   // + two idx tiles, two dup-flag tiles
+template <int T> constexpr size_t cpi_smem() { return cp_smem<T>() + (size_t)2 * T * 32; }   // + two idx tiles
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
@@ -780,9 +780,13 @@ __global__ void __launch_bounds__(Body::THREADS, Body::MINB)
     int32_t* const rows = reinterpret_cast<int32_t*>(cp_buf + 2 * 24 * CP_THREADS);
     int32_t* const row0 = rows + 8 * tid;                     // id row of tiles with even k
     int32_t* const row1 = rows + 8 * (CP_THREADS + tid);      // ... odd k
-    uint8_t* const dupf = reinterpret_cast<uint8_t*>(rows + 16 * CP_THREADS);
-    uint8_t* const dup0 = dupf + tid;                         // duplicate-id flag of tiles with even k
-    uint8_t* const dup1 = dupf + CP_THREADS + tid;            // ... odd k
+    // duplicate-id flags of tiles with even / odd k in a static array: their shared address
+    // is a link-time constant plus tid, which the compiler rematerializes on the slow path
+    // (a dynamic-smem base kept across the compute went to the stack frame and its reload
+    // was the kernel's hottest stall, 6.6% of the samples on config 3)
+    __shared__ uint8_t s_dup[2][CP_THREADS];
+    uint8_t* const dup0 = &s_dup[0][tid];
+    uint8_t* const dup1 = &s_dup[1][tid];
     const uint32_t r0 = smem_u32(row0), r1 = smem_u32(row1);
     int t = blockIdx.x;
     auto hex_of = [&](int tile) { return (int64_t)tile * CP_THREADS + tid; };

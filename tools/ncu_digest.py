@@ -43,10 +43,26 @@ def main():
             if k in r:
                 print(f"  {k} = {r[k]}")
     if nsrc:
+        # SASS view: row 0 names the kernel, row 1 is the header, then one row per instruction
         src = list(csv.reader(io.StringIO(ncu([rep, "--page", "source", "--csv", "--print-source", "sass"]))))
-        if src:
-            hdr = src[0]
-            print("\nsource columns:", hdr[:12])
+        if len(src) > 2:
+            hdr = src[1]
+            ix = {h: i for i, h in enumerate(hdr)}
+            stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+            rows, total = [], 0
+            for r in src[2:]:
+                try:
+                    smp = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+                    ex = int(r[ix["Instructions Executed"]] or 0)
+                except (ValueError, IndexError, KeyError):
+                    continue
+                total += smp
+                top = sorted(((int(r[ix[c]] or 0), c[6:]) for c in stall_cols), reverse=True)[:2]
+                rows.append((smp, ex, r[ix["Address"]][-5:], r[ix["Source"]].strip()[:64], top))
+            print(f"\ntop {nsrc} SASS lines by stall samples (share of {total} samples; warp-level executions):")
+            for smp, ex, addr, text, top in sorted(rows, reverse=True)[:nsrc]:
+                why = " ".join(f"{c}:{v * 100 // max(smp, 1)}%" for v, c in top if v)
+                print(f"  {100.0 * smp / max(total, 1):5.2f}%  {ex:>12d}  {addr}  {text:64s}  {why}")
 
 
 if __name__ == "__main__":
