@@ -94,7 +94,7 @@ def parse():
                         "bounds: NEXT-1 certified min det J bounds; select: NEXT-3 candidate filtering "
                         "(on the config's flags); quads: NEXT-4 linear quadrangles (10M, noise 0.35)")
     p.add_argument("--rel-tol", type=float, default=1e-3, help="NEXT-1 tolerance (relative to max|b|)")
-    p.add_argument("--variant", choices=["ldg", "wtma", "cp"], default=None,
+    p.add_argument("--variant", choices=["ldg", "wtma", "cp", "bulk"], default=None,
                    help="pass-1 kernel variant for SoA inputs (sets HEXVAL_PASS1; default: the library's)")
     args = p.parse_args()
     if args.variant:

@@ -724,6 +724,98 @@ __global__ void __launch_bounds__(Body::THREADS, Body::MINB)
     body.finish();
 }
 
+// K1 (bulk variant, HEXVAL_PASS1=bulk): the CTA's 256-hex tile is staged by 24
+// bulk copies of 2 KB (one per coordinate plane, issued by lanes 0-23 of warp 0)
+// completing on a per-stage "full" mbarrier; each warp reads its hexes, arrives on
+// the stage's "empty" mbarrier, and warp 0 refills a stage once all 8 warps have
+// read it.  Per hex this replaces 24 8-byte cp.async copies and their 64-bit
+// address arithmetic (~72 instructions per warp tile) by ~10; small (256-B, one per
+// warp) bulk copies are bound by the copy engine's request rate (wtma variant).
+// Full tiles only; the ragged tail (n mod 256 hexes) is done with plain loads.
+// Measured on config 1 (profiles/r02/PASS1_EXPERIMENTS.md): 344 us vs 329 us for the
+// per-thread cp.async pipeline -- the fewer instructions do not pay for coupling the
+// CTA's 8 warps to one refill; kept as a tuning alternative.
+constexpr int BK_THREADS = 256;
+constexpr int BK_ROW = BK_THREADS + 2;            // doubles per staged plane: 256 + one element of shift, rounded to 16 B
+constexpr int BK_STAGE = 24 * BK_ROW;             // doubles per stage
+constexpr size_t BK_SMEM = (size_t)2 * BK_STAGE * sizeof(double);
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// warp 0: stage tile t (hexes 256t .. 256t+255, all < n) into buf; plane p starts at element
+// e = p n + 256 t, copied from e - (e & 1) (16-B aligned: coords is 16-B aligned on this path)
+__device__ __forceinline__ void bk_issue(const double* __restrict__ coords, int64_t n, int t, double* buf,
+                                         uint64_t* full, int lane) {
+    const bool odd = n & 1;
+    if (lane == 0) mbar_expect_tx(full, odd ? 12u * 2064u + 12u * 2048u : 24u * 2048u);
+    __syncwarp();
+    if (lane < 24) {
+        const int64_t e = (int64_t)lane * n + (int64_t)t * BK_THREADS;
+        const uint64_t policy = policy_evict_first();
+        if (e & 1) bulk_g2s(buf + lane * BK_ROW, coords + e - 1, 2064u, full, policy);
+        else bulk_g2s(buf + lane * BK_ROW, coords + e, 2048u, full, policy);
+    }
+}
+
+template <class Body>
+__global__ void __launch_bounds__(BK_THREADS, 2)
+    soa_bulk_kernel(const double* __restrict__ coords, int64_t n, Body body) {
+    extern __shared__ __align__(128) double bk_buf[];        // [2][24][BK_ROW]
+    __shared__ __align__(8) uint64_t full[2], empty[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tiles = (int)(n / BK_THREADS);                 // full tiles
+    const int G = (int)gridDim.x;
+    const int shift = (int)(n & 1);                          // odd planes start one element into their row
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&empty[0], BK_THREADS / 32);
+        mbar_init(&empty[1], BK_THREADS / 32);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    int t = blockIdx.x;
+    if (warp == 0) {
+        if (t < tiles) bk_issue(coords, n, t, bk_buf, &full[0], lane);
+        if (t + G < tiles) bk_issue(coords, n, t + G, bk_buf + BK_STAGE, &full[1], lane);
+    }
+    for (int k = 0; t < tiles; t += G, ++k) {
+        const int b = k & 1;
+        const unsigned ph = (unsigned)((k >> 1) & 1);
+        mbar_wait(&full[b], ph);
+        const double* src = bk_buf + b * BK_STAGE + tid;
+        double X[24];
+#pragma unroll
+        for (int p = 0; p < 24; ++p) X[p] = src[p * BK_ROW + (shift & p)];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[b]);                // this warp has read stage b
+        // refill before computing: the warps read a stage together once it lands (refilling
+        // after the compute measured 344.5 vs 343.9 us and spilled 20 B)
+        if (warp == 0 && t + 2 * G < tiles) {
+            mbar_wait(&empty[b], ph);                        // every warp has read stage b
+            bk_issue(coords, n, t + 2 * G, bk_buf + b * BK_STAGE, &full[b], lane);
+        }
+        const int64_t i = (int64_t)t * BK_THREADS + tid;
+        const int st = body.hex(SoaLoader{coords, n}, X, i);
+        body.epilogue(st, i);
+    }
+    // ragged tail: the block that would own tile `tiles` does the last n mod 256 hexes with plain loads
+    if ((int64_t)tiles * BK_THREADS < n && blockIdx.x == tiles % G) {
+        const int64_t i = (int64_t)tiles * BK_THREADS + tid;
+        int st = -1;
+        if (i < n) {
+            double X[24];
+#pragma unroll
+            for (int p = 0; p < 24; ++p) X[p] = __ldcs(coords + (int64_t)p * n + i);
+            st = body.hex(SoaLoader{coords, n}, X, i);
+        }
+        body.epilogue(st, i);
+    }
+    body.finish();
+}
+
 // K2 (cp.async variant): the same pipeline for int32 connectivity, three deep:
 // while a thread computes its hex of tile k, the coordinates of its hex in
 // tile k+1 are in flight (gathered with async copies from the vertex array,
@@ -1957,12 +2049,33 @@ int cp_setup(int* screen_ctas) {
     return occ;
 }
 
-// Pass-1 variant for SoA inputs: HEXVAL_PASS1 = ldg | wtma | cp (tuning knob
+template <class Body>
+bool bulk_attr() {
+    return cudaFuncSetAttribute((const void*)soa_bulk_kernel<Body>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)BK_SMEM) == cudaSuccess;
+}
+int bulk_setup() {
+    if (!(bulk_attr<Pass1Body<false, false>>() && bulk_attr<Pass1Body<false, true>>() &&
+          bulk_attr<Pass1Body<true, false>>() && bulk_attr<Pass1Body<true, true>>())) {
+        cudaGetLastError();
+        return 0;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, soa_bulk_kernel<Pass1Body<false, false>>, BK_THREADS,
+                                                      BK_SMEM) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return occ;
+}
+
+// Pass-1 variant for SoA inputs: HEXVAL_PASS1 = ldg | wtma | cp | bulk (tuning knob
 // for measurements).
-enum { P1_LDG = 0, P1_WTMA = 1, P1_CP = 2 };
+enum { P1_LDG = 0, P1_WTMA = 1, P1_CP = 2, P1_BULK = 3 };
 int pass1_variant_from_env() {
     const char* v = getenv("HEXVAL_PASS1");
     if (v && !strcmp(v, "wtma")) return P1_WTMA;
+    if (v && !strcmp(v, "bulk")) return P1_BULK;
     if (v && !strcmp(v, "cp")) return P1_CP;
     if (v && !strcmp(v, "ldg")) return P1_LDG;
     return P1_CP;                 // measured best on B200 (profiles/r01)
@@ -1979,7 +2092,8 @@ const DeviceInfo& device_info(int dev) {
                                                       0);
         d.k4_blocks_per_sm = occ > 0 ? occ : 1;
         const int want = pass1_variant_from_env();
-        const int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP ? cp_setup(&d.screen_ctas_per_sm) : 0);
+        int ctas = want == P1_WTMA ? wtma_setup() : (want == P1_CP || want == P1_BULK ? cp_setup(&d.screen_ctas_per_sm) : 0);
+        if (want == P1_BULK && ctas > 0) ctas = bulk_setup();
         d.p1_variant = ctas > 0 ? want : P1_LDG;
         d.p1_ctas_per_sm = ctas > 0 ? ctas : 1;
         d.ok = true;
@@ -2052,6 +2166,13 @@ void launch_pass1<IdxLoader>(const IdxLoader& ld, const DeviceInfo& info, const 
     });
 }
 
+void launch_bulk(const SoaLoader& ld, const DeviceInfo& info, const P1Args& a, cudaStream_t stream) {
+    const int64_t tiles = (a.n + BK_THREADS - 1) / BK_THREADS;
+    const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
+    const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+    with_pass1_body(a, [&](auto body) { soa_bulk_kernel<<<grid, BK_THREADS, BK_SMEM, stream>>>(ld.coords, a.n, body); });
+}
+
 void launch_wtma(const SoaLoader& ld, const DeviceInfo& info, const P1Args& a, cudaStream_t stream) {
     const int64_t chunks = (a.n + 31) / 32;
     const int64_t cap = (int64_t)info.sms * info.p1_ctas_per_sm;
@@ -2084,7 +2205,8 @@ template <>
 void launch_pass1<SoaLoader>(const SoaLoader& ld, const DeviceInfo& info, const P1Args& a, cudaStream_t stream) {
     const bool aligned = (((uintptr_t)ld.coords) & 15) == 0;
     if (aligned && info.p1_variant == P1_WTMA && !a.sj) launch_wtma(ld, info, a, stream);
-    else if (info.p1_variant == P1_CP) launch_cp(ld, info, a, stream);
+    else if (aligned && info.p1_variant == P1_BULK && !a.sj) launch_bulk(ld, info, a, stream);
+    else if (info.p1_variant == P1_CP || info.p1_variant == P1_BULK) launch_cp(ld, info, a, stream);
     else launch_pass1_plain(ld, a, stream);
 }
 

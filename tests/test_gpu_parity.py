@@ -348,11 +348,12 @@ def test_indexed_misaligned_pointers_same_results(shift_idx, shift_verts):
     assert np.array_equal(f.cpu().numpy(), ref_f) and np.array_equal(k.cpu().numpy(), ref_k)
 
 
-def test_pass1_variants_bit_identical(tmp_path):
-    """HEXVAL_PASS1=ldg|wtma|cp (tuning knob) give identical flags and coefficients."""
+@pytest.mark.parametrize("n", [256 * 148 * 2 + 77, 256 * 148 * 3 + 256 * 5])
+def test_pass1_variants_bit_identical(tmp_path, n):
+    """HEXVAL_PASS1=ldg|wtma|cp|bulk (tuning knob) give identical flags and coefficients
+    (odd n: shifted plane rows and a ragged tail; even n: full tiles only)."""
     import subprocess
     import sys
-    n = 256 * 148 * 2 + 77
     coords = hexgen.ragged_soa(n, seed=5, amp=0.5)
     np.save(tmp_path / "c.npy", coords)
     script = (
@@ -363,11 +364,11 @@ def test_pass1_variants_bit_identical(tmp_path):
         "f, k = hv.check_soa(c, coeffs=True); torch.cuda.synchronize()\n"
         f"np.save({str(tmp_path)!r} + '/f_' + sys.argv[1] + '.npy', f.cpu().numpy())\n"
         f"np.save({str(tmp_path)!r} + '/k_' + sys.argv[1] + '.npy', k.cpu().numpy())\n")
-    for v in ("ldg", "wtma", "cp"):
+    for v in ("ldg", "wtma", "cp", "bulk"):
         env = dict(os.environ, HEXVAL_PASS1=v)
         subprocess.run([sys.executable, "-c", script, v], env=env, check=True, timeout=300)
     f0, k0 = np.load(tmp_path / "f_ldg.npy"), np.load(tmp_path / "k_ldg.npy")
-    for v in ("wtma", "cp"):
+    for v in ("wtma", "cp", "bulk"):
         assert np.array_equal(np.load(tmp_path / f"f_{v}.npy"), f0), v
         assert np.array_equal(np.load(tmp_path / f"k_{v}.npy"), k0), v
 
