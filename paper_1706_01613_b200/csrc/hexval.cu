@@ -1244,6 +1244,7 @@ struct K4Warp {
 // pop size is then known without a shared-memory round trip, and the next
 // nonempty level is one ballot away (profiles/r02/K4_EXPERIMENTS.md: the
 // shared-memory counters' load-use chains were 8% of the kernel's stall samples).
+static_assert(MAX_DEPTH < 32, "one lane per stack level");
 struct LevelCounts {
     int tcnt = 0, lcnt = 0;
     // after a step at level d (the top level) that pushed `pushed` nodes at level d+1
