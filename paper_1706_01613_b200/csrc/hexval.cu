@@ -356,12 +356,20 @@ __device__ __forceinline__ double corner_sj(const V3* E, const double* c) {
                          __dmul_rn(__dmul_rn(l56, l58), l15), __dmul_rn(__dmul_rn(l56, l67), l26),
                          __dmul_rn(__dmul_rn(l87, l67), l37), __dmul_rn(__dmul_rn(l87, l58), l48)};
     double bn = __dmul_rn(c[0], fabs(c[0])), bp = P[0], bc = c[0];
-    bool zero_edge = !(P[0] > 0.0);
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
-        zero_edge |= !(P[k] > 0.0);
         const double nk = __dmul_rn(c[k], fabs(c[k]));
         if (__dmul_rn(nk, bp) < __dmul_rn(bn, P[k])) { bn = nk; bp = P[k]; bc = c[k]; }   // nk/P[k] < bn/bp
+    }
+    // a zero-length corner edge (P == 0): P >= 0 always, and a positive high word proves
+    // P > 0, so the FP64 compares run only when some P is 0 or below 2^-1042 (rare)
+    int pk = key(P[0]);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) pk = min(pk, key(P[k]));
+    bool zero_edge = false;
+    if (pk <= 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) zero_edge |= !(P[k] > 0.0);
     }
     // the winner's c / sqrt(P) as c * rsqrt(P) (a few ulps; the parity tolerance is 1e-13)
     return zero_edge ? __longlong_as_double(0x7ff8000000000000ll) : __dmul_rn(bc, rsqrt(bp));
