@@ -910,6 +910,14 @@ def test_select_valid_parity(n):
         ids2, c2, _ = hv.select_valid(f[1:])
         torch.cuda.synchronize()
         assert np.array_equal(ids2.cpu().numpy(), oracle.select_valid(flags[1:])[0])
+        # flags and group views offset by one element: the group ids no longer take the
+        # 16-B vector loads (scalar fallback) and the staged ordered write starts mid-row
+        ids3, c3, counts3 = hv.select_valid(f[1:], g[1:], 1000)
+        torch.cuda.synchronize()
+        ref3_ids, ref3_counts = oracle.select_valid(flags[1:], group[1:], 1000)
+        assert c3 == ref3_ids.size
+        assert np.array_equal(ids3.cpu().numpy(), ref3_ids)
+        assert np.array_equal(counts3.cpu().numpy(), ref3_counts)
 
 
 def test_select_valid_config3_pipeline():
