@@ -355,12 +355,27 @@ __device__ __forceinline__ double corner_sj(const V3* E, const double* c) {
                          __dmul_rn(__dmul_rn(l43, l23), l37), __dmul_rn(__dmul_rn(l43, l14), l48),
                          __dmul_rn(__dmul_rn(l56, l58), l15), __dmul_rn(__dmul_rn(l56, l67), l26),
                          __dmul_rn(__dmul_rn(l87, l67), l37), __dmul_rn(__dmul_rn(l87, l58), l48)};
+#ifdef HEXVAL_SJ_TOURNAMENT
+    // argmin of c_k |c_k| / P_k as a three-round tournament (the lower index wins a tie, as in
+    // the sequential scan; seven cross-multiplied compares either way, but a dependency chain of
+    // three instead of seven)
+    double N[8], Q[8], C[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { N[k] = __dmul_rn(c[k], fabs(c[k])); Q[k] = P[k]; C[k] = c[k]; }
+#pragma unroll
+    for (int h = 1; h < 8; h *= 2)
+#pragma unroll
+        for (int k = 0; k < 8; k += 2 * h)
+            if (__dmul_rn(N[k + h], Q[k]) < __dmul_rn(N[k], Q[k + h])) { N[k] = N[k + h]; Q[k] = Q[k + h]; C[k] = C[k + h]; }
+    const double bp = Q[0], bc = C[0];
+#else
     double bn = __dmul_rn(c[0], fabs(c[0])), bp = P[0], bc = c[0];
 #pragma unroll
     for (int k = 1; k < 8; ++k) {
         const double nk = __dmul_rn(c[k], fabs(c[k]));
         if (__dmul_rn(nk, bp) < __dmul_rn(bn, P[k])) { bn = nk; bp = P[k]; bc = c[k]; }   // nk/P[k] < bn/bp
     }
+#endif
     // a zero-length corner edge (P == 0): P >= 0 always, and a positive high word proves
     // P > 0, so the FP64 compares run only when some P is 0 or below 2^-1042 (rare)
     int pk = key(P[0]);
