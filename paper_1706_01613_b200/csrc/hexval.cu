@@ -1024,17 +1024,46 @@ __device__ __noinline__ uint8_t exact_resolve(const double* X) {
 // nodes of the same depth (the top level of the stack) into their 8 children
 // (de Casteljau at t = 1/2 per axis, reading G3), classify each child
 // and push the undecided ones with a warp prefix sum.
-// Only nodes of one depth are popped per step and their children are pushed on
-// top, so the stack is sorted by depth and holds at most 32 x 8 = 256 nodes per
-// level: K4_CAP = 19 x 256 nodes (levels 1..19; children at depth 20 are
-// classified but never pushed, reading G5).  Per-hex state (INVALID / depth
-// cap reached) lives in shared memory; nodes of a hex already found INVALID
-// are dropped (the paper's early return).
+// Only nodes of one depth are popped per step (the top level of the stack) and
+// their children are pushed on top, so the stack is sorted by depth.  Children
+// at depth 20 are classified but never pushed (reading G5).  Per-hex state
+// (INVALID / depth cap reached) lives in shared memory; nodes of a hex already
+// found INVALID are dropped (the paper's early return).
+//
+// Stack capacity.  A step that pops k nodes pushes at most 8k, so the height h
+// grows by at most 7k.  The pop size is capacity-adaptive (pop_size): with
+// K4_TM = K4_CAP - K4_RESERVE, a normal step takes k = min(32, top-level count,
+// (K4_TM - h) / 7) nodes and ends with h <= K4_TM; when not even one node fits
+// under K4_TM the step pops exactly one node.  A run of such one-node steps is
+// plain depth-first search from a state with h0 <= K4_TM (the state after a
+// normal step, or a fresh batch of <= 32 roots): the nodes of that state only get
+// consumed, and the run adds at most 7 unexpanded siblings per deeper level, so
+// h <= h0 + 7 * (MAX_DEPTH - 1) < K4_TM + K4_RESERVE = K4_CAP throughout, and the
+// run ends as soon as a node fits under K4_TM again.  Every step pops at least one
+// node, so the traversal always progresses; the capacity only bounds how wide it
+// runs.  Measured on config 4 (profiles/r02/s4): K4_CAP = 1024 (229 KB per warp, 271 MB per
+// arena) runs at the speed and lane use (0.837) of the unconditional worst case reserved
+// before (19 levels x 256 nodes = 4864 slots, 1.3 GB per arena); 512 slots throttle the
+// pops (lane use 0.42, 422 ms vs 252 ms), 416 more so (0.26, 626 ms) -- still correct: the
+// whole GPU suite passes with HEXVAL_K4_CAP=416 and the invariant traps on.
 constexpr int K4_WARPS = K4_THREADS / 32;
-constexpr int K4_CAP = (MAX_DEPTH - 1) * 256;
+#ifndef HEXVAL_K4_CAP
+#define HEXVAL_K4_CAP 1024
+#endif
+constexpr int K4_CAP = HEXVAL_K4_CAP;
+constexpr int K4_RESERVE = 7 * MAX_DEPTH;
+constexpr int K4_TM = K4_CAP - K4_RESERVE;
+static_assert(K4_TM >= 8 * 32, "a batch of 32 roots and their 256 children fit under the threshold");
+static_assert(K4_CAP % 4 == 0, "128-byte lines hold 4 slots of one vector");
+constexpr int K4_STRIDE = K4_CAP;   // slots between the 7 vector planes of a warp's stack (padding measured: no effect)
+
+// nodes to pop from a stack of height h whose top level holds tcnt nodes
+__device__ __forceinline__ int pop_size(int tcnt, int h) {
+    return min(min(32, tcnt), max(1, (K4_TM - h) / 7));
+}
 
 struct WarpStacks {
-    double* coef;           // [warp][7][K4_CAP][4]: 32-byte vectors of a node's 28 values (27 coefficients
+    double* coef;           // [warp][7][K4_STRIDE][4]: 32-byte vectors of a node's 28 values (27 coefficients
                             // in layout i + 3j + 9k, then the node's meta word)
 };
 
@@ -1076,7 +1105,7 @@ __device__ __forceinline__ void discard_popped(const double* sc, int lo, int k, 
     for (int r = 0; r < 2; ++r) {
         const int idx = lane + 32 * r, q = idx >> 3, j = idx & 7;
         if (q < 7 && j < nl)
-            asm volatile("discard.global.L2 [%0], 128;" ::"l"(sc + ((size_t)q * K4_CAP + 4 * (f + j)) * 4) : "memory");
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(sc + ((size_t)q * K4_STRIDE + 4 * (f + j)) * 4) : "memory");
     }
 #endif
 }
@@ -1088,34 +1117,35 @@ __device__ __forceinline__ unsigned long long stack_load(const double* sc, int s
     double m;
 #pragma unroll
     for (int q = 0; q < 7; ++q) {
-        const double* src = sc + ((size_t)q * K4_CAP + slot) * 4;
+        const double* src = sc + ((size_t)q * K4_STRIDE + slot) * 4;
         if (q < 6) ld_v4(src, P[4 * q], P[4 * q + 1], P[4 * q + 2], P[4 * q + 3]);
         else ld_v4(src, P[24], P[25], P[26], m);
     }
     return (unsigned long long)__double_as_longlong(m);
 }
 __device__ __forceinline__ void stack_store_if(bool on, double* sc, int slot, const double* C, unsigned long long meta) {
-    // one predicate for the node's 7 vector stores (offsets: K4_CAP * 32 bytes per vector)
+    // one predicate for the node's 7 vector stores (offsets: K4_STRIDE * 32 bytes per vector)
     double* dst = sc + (size_t)slot * 4;
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %29, 0;\n\t"
                  "@q " HV_ST_V4 " [%0], {%1,%2,%3,%4};\n\t"
-                 "@q " HV_ST_V4 " [%0+155648], {%5,%6,%7,%8};\n\t"
-                 "@q " HV_ST_V4 " [%0+311296], {%9,%10,%11,%12};\n\t"
-                 "@q " HV_ST_V4 " [%0+466944], {%13,%14,%15,%16};\n\t"
-                 "@q " HV_ST_V4 " [%0+622592], {%17,%18,%19,%20};\n\t"
-                 "@q " HV_ST_V4 " [%0+778240], {%21,%22,%23,%24};\n\t"
-                 "@q " HV_ST_V4 " [%0+933888], {%25,%26,%27,%28};\n\t}"
+                 "@q " HV_ST_V4 " [%0+%30], {%5,%6,%7,%8};\n\t"
+                 "@q " HV_ST_V4 " [%0+%31], {%9,%10,%11,%12};\n\t"
+                 "@q " HV_ST_V4 " [%0+%32], {%13,%14,%15,%16};\n\t"
+                 "@q " HV_ST_V4 " [%0+%33], {%17,%18,%19,%20};\n\t"
+                 "@q " HV_ST_V4 " [%0+%34], {%21,%22,%23,%24};\n\t"
+                 "@q " HV_ST_V4 " [%0+%35], {%25,%26,%27,%28};\n\t}"
                  ::"l"(dst), "d"(C[0]), "d"(C[1]), "d"(C[2]), "d"(C[3]), "d"(C[4]), "d"(C[5]), "d"(C[6]), "d"(C[7]),
                  "d"(C[8]), "d"(C[9]), "d"(C[10]), "d"(C[11]), "d"(C[12]), "d"(C[13]), "d"(C[14]), "d"(C[15]),
                  "d"(C[16]), "d"(C[17]), "d"(C[18]), "d"(C[19]), "d"(C[20]), "d"(C[21]), "d"(C[22]), "d"(C[23]),
-                 "d"(C[24]), "d"(C[25]), "d"(C[26]), "d"(__longlong_as_double((long long)meta)), "r"((unsigned)on)
+                 "d"(C[24]), "d"(C[25]), "d"(C[26]), "d"(__longlong_as_double((long long)meta)), "r"((unsigned)on),
+                 "n"(1 * K4_STRIDE * 32), "n"(2 * K4_STRIDE * 32), "n"(3 * K4_STRIDE * 32), "n"(4 * K4_STRIDE * 32),
+                 "n"(5 * K4_STRIDE * 32), "n"(6 * K4_STRIDE * 32)
                  : "memory");
 }
-static_assert(K4_CAP * 32 == 155648, "stack_store_if's vector offsets");
 __device__ __forceinline__ void stack_store(double* sc, int slot, const double* C, unsigned long long meta) {
 #pragma unroll
     for (int q = 0; q < 7; ++q) {
-        double* dst = sc + ((size_t)q * K4_CAP + slot) * 4;
+        double* dst = sc + ((size_t)q * K4_STRIDE + slot) * 4;
         if (q < 6) st_v4(dst, C[4 * q], C[4 * q + 1], C[4 * q + 2], C[4 * q + 3]);
         else st_v4(dst, C[24], C[25], C[26], __longlong_as_double((long long)meta));
     }
@@ -1366,7 +1396,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
     const int lane = threadIdx.x & 31;
     K4Warp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
-    double* const sc = ws.coef + gw * 28 * K4_CAP;
+    double* const sc = ws.coef + gw * 28 * K4_STRIDE;
     const unsigned total = *((volatile unsigned*)&ctl->n_sub);
     const unsigned n_exact = *((volatile unsigned*)&ctl->n_exact);
     bool ex_left = n_exact > 0;                          // warp-uniform: the exact queue may hold items
@@ -1440,7 +1470,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             __syncwarp();
         }
         {
-            const int k = min(32, lc.tcnt);
+            const int k = pop_size(lc.tcnt, top);
             HV_CHECK(D >= 0 && D < MAX_DEPTH && k > 0 && k <= top);
             act = lane < k;
             d = D;
@@ -1663,7 +1693,7 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
     const int lane = threadIdx.x & 31;
     BWarp& W = wst[threadIdx.x >> 5];
     const size_t gw = (size_t)blockIdx.x * K4_WARPS + (threadIdx.x >> 5);
-    double* const sc = ws.coef + gw * 28 * K4_CAP;
+    double* const sc = ws.coef + gw * 28 * K4_STRIDE;
     const unsigned lt_mask = (1u << lane) - 1u;
     LevelCounts lc;
     int top = 0, D = 0, nb = 0;
@@ -1706,7 +1736,7 @@ __global__ void HV_K4_BOUNDS bounds_kernel(L ld, double rel_tol, double* __restr
                 act = true;                                  // queued: the root is split
             }
         } else {
-            const int k = min(32, lc.tcnt);
+            const int k = pop_size(lc.tcnt, top);
             HV_CHECK(D > 0 && D < MAX_DEPTH && k > 0 && k <= top);
             d = D;
             if (lane < k) {
@@ -2278,7 +2308,7 @@ int run_device(const L& ld, int64_t n, uint8_t* flags, double* coeffs, hexval_st
     if (prof && prof->count >= hexval_profile::CAP) return HEXVAL_ERR_ARGUMENT;   // read it first
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
-    const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
+    const size_t sc_bytes = warps * 28 * K4_STRIDE * sizeof(double);
     const size_t total = ctl_bytes + 2 * q_bytes + sc_bytes;
     hexval_scratch::Lease lease;
     if (hexval_scratch::acquire(lease, total, stream) != cudaSuccess) {
@@ -2352,7 +2382,7 @@ int run_bezier(const double* b, int64_t n, uint8_t* flags, hexval_stats* stats, 
     const size_t warps = (size_t)k4_blocks * K4_WARPS;
     const size_t ctl_bytes = 256;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
-    const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
+    const size_t sc_bytes = warps * 28 * K4_STRIDE * sizeof(double);
     hexval_scratch::Lease lease;
     if (hexval_scratch::acquire(lease, ctl_bytes + q_bytes + sc_bytes, stream) != cudaSuccess) {
         cudaGetLastError();
@@ -2394,7 +2424,7 @@ int run_bounds(const L& ld, int64_t n, double rel_tol, double* lower, double* up
     const int64_t blocks = k4_grid(info, n, occ);
     const size_t warps = (size_t)blocks * K4_WARPS;
     const size_t q_bytes = ((size_t)n * 4 + 255) & ~(size_t)255;
-    const size_t sc_bytes = warps * 28 * K4_CAP * sizeof(double);
+    const size_t sc_bytes = warps * 28 * K4_STRIDE * sizeof(double);
     hexval_scratch::Lease lease;
     if (hexval_scratch::acquire(lease, 256 + q_bytes + sc_bytes, stream) != cudaSuccess) {
         cudaGetLastError();
