@@ -145,6 +145,24 @@ __device__ __forceinline__ bool out_of_range(const double* X) {
     for (int p = 0; p < 24; ++p) bad |= !(fabs(X[p]) <= 0x1p300);
     return bad;
 }
+// The same test for a hex whose edge-scale key is known (pass 1): every node is joined to
+// node 1 by at most 3 hex edges, so edge components and node-1 coordinates all below 2^297
+// put every |x| below 2^297 (1 + 3 (1 + 2u)) < 2^300 (the computed components are within a
+// factor 1 + u of the true differences), and a NaN or Inf coordinate makes the components of
+// its 3 edges NaN or Inf (key >= 0x7ff00000).  3 masked keys instead of 24 on the fast path
+// (k1 = max abskey of node 1, taken before the samples so that X need not stay live); the
+// slow path re-reads the hex and runs the exact test, out of line.
+template <class L>
+__device__ __noinline__ bool out_of_range_slow(const L ld, int64_t i) {
+    double X[24];
+    ld.load(i, X);
+    bool bad = false;
+#pragma unroll
+    for (int p = 0; p < 24; ++p) bad |= !(fabs(X[p]) <= 0x1p300);
+    return bad;
+}
+__device__ __forceinline__ int node1_key(const double* X) { return max(abskey(X[0]), max(abskey(X[1]), abskey(X[2]))); }
+constexpr int RANGE_FAST_KEY = 0x52800000;               // 2^297
 
 // Two nodes that share a face coincide (exact double equality of all three
 // coordinates) => some Step-2 sample is exactly 0 => INVALID (reading G2):
@@ -255,15 +273,18 @@ __device__ __forceinline__ int step2_class(const Samples& s, double tau2) {
     }
     // Integer pipe, conservative in the hi words: a sample is robustly negative
     // if its sign is set and its hi word exceeds that of tau2 (then |x| > tau2);
-    // it is ambiguous if |x|'s hi word <= that of tau2.
-    unsigned um = 0;
-    int am = 0x7fffffff;
+    // it is ambiguous if |x|'s hi word <= that of tau2.  Here km <= T, so once no
+    // sample is robustly negative some sample is ambiguous: either a key is negative
+    // -- then um is the largest such key and um <= (sign | T) puts every negative
+    // sample's |x| hi word at or below T -- or all keys are >= 0 and km is the
+    // smallest |x| hi word.  No minimum over the masked keys is needed (session 4:
+    // 20 LOP3 + 10 VIMNMX3 fewer per hex on the indexed path).
+    unsigned um = (unsigned)key(s.c[0]);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) { um = max(um, (unsigned)key(s.c[k])); am = min(am, abskey(s.c[k])); }
+    for (int k = 1; k < 8; ++k) um = max(um, (unsigned)key(s.c[k]));
 #pragma unroll
-    for (int e = 0; e < 12; ++e) { um = max(um, (unsigned)key(s.d[e])); am = min(am, abskey(s.d[e])); }
-    if (um > (0x80000000u | (unsigned)T)) return ST_INVALID;   // some sample robustly negative
-    return am <= T ? ST_EXACT : ST_VALID;
+    for (int e = 0; e < 12; ++e) um = max(um, (unsigned)key(s.d[e]));
+    return um > (0x80000000u | (unsigned)T) ? ST_INVALID : ST_EXACT;
 }
 
 __device__ __forceinline__ void write_coeffs(double* __restrict__ coeffs, int64_t n, int64_t i,
@@ -453,29 +474,61 @@ __device__ __noinline__ QualOut quality_slow(const L ld, int64_t i, double sj, u
 // S1-S5 + S8 for one hex whose 24 coordinates are in registers; returns the
 // pass-1 state (ST_*).
 // QUAL: also the fused NEXT-2 screening outputs (corner_quality) of the hex.
-template <bool COEFFS, class L, bool QUAL = false>
+template <bool COEFFS, class L, bool QUAL = false, bool FAST_RANGE = true>
 __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i, int64_t n,
                                          uint8_t* __restrict__ flags, double* __restrict__ coeffs,
                                          double* __restrict__ sj_out = nullptr, uint8_t* __restrict__ t1_out = nullptr) {
     int st;
     double sj = __longlong_as_double(0x7ff8000000000000ll);
     uint8_t t1 = 0;
-    if (out_of_range(X)) {
-        st = ST_NONFINITE;
-    } else {
+    if constexpr (QUAL && FAST_RANGE) {
+        // the fused screening kernels (166 registers, not at a register cliff) take the
+        // NONFINITE test from the edge-scale key: 3 masked keys instead of 24 per hex
+        // (399.2 -> 391.7 us on config 1).  In the validity kernels, which sit at 128
+        // registers, the same reordering spilled loop state (328 -> 358 us): they keep
+        // the test on the 24 coordinates up front.
         Samples s;
-        if (QUAL) samples20(X, s, [&](const V3* E, const double* c, int ek) { corner_quality(E, c, ek, sj, t1); });
-        else samples20(X, s);                             // S1 + S2
+        s.range_key = node1_key(X);                           // samples20 folds the edge-scale key into it
+        samples20(X, s, [&](const V3* E, const double* c, int ek) { corner_quality(E, c, ek, sj, t1); });   // S1 + S2
+        // NONFINITE (reading G13) is decided last, when little is live across the out-of-line
+        // exact test; until then a suspect hex (possibly NaN / out-of-range samples) only goes
+        // through the register arithmetic below, never through the exact-sign machinery
+        const bool suspect = s.suspect;
         st = step2_class<L::kIntStep2>(s, step2_tau(s.ekey));   // S3 (Step 2)
         if (st == ST_EXACT && ld.dup_face_pair(i)) st = ST_INVALID;   // a sample is exactly 0
-        Coeffs t;
-        transform(s, t);                                  // S4 (Step 3)
-        if (st == ST_VALID && !step4_positive(t)) st = ST_SUB;   // S5 (Step 4)
-        if (COEFFS) write_coeffs(coeffs, n, i, s, t);
-        if (QUAL && (t1 & (SJ_RESCALE | T1_PENDING))) {
+        {
+            Coeffs t;
+            transform(s, t);                                  // S4 (Step 3)
+            if (st == ST_VALID && !step4_positive(t)) st = ST_SUB;   // S5 (Step 4)
+            if (COEFFS) write_coeffs(coeffs, n, i, s, t);
+        }
+        if (suspect && out_of_range_slow(ld, i)) {
+            st = ST_NONFINITE;
+            sj = __longlong_as_double(0x7ff8000000000000ll);
+            t1 = 0;
+        } else if (t1 & (SJ_RESCALE | T1_PENDING)) {
             const QualOut q = quality_slow(ld, i, sj, t1);
             sj = q.sj;
             t1 = (uint8_t)q.t1;
+        }
+    } else {
+        if (out_of_range(X)) {
+            st = ST_NONFINITE;
+        } else {
+            Samples s;
+            if (QUAL) samples20(X, s, [&](const V3* E, const double* c, int ek) { corner_quality(E, c, ek, sj, t1); });
+            else samples20(X, s);                             // S1 + S2
+            st = step2_class<L::kIntStep2>(s, step2_tau(s.ekey));   // S3 (Step 2)
+            if (st == ST_EXACT && ld.dup_face_pair(i)) st = ST_INVALID;   // a sample is exactly 0
+            Coeffs t;
+            transform(s, t);                                  // S4 (Step 3)
+            if (st == ST_VALID && !step4_positive(t)) st = ST_SUB;   // S5 (Step 4)
+            if (COEFFS) write_coeffs(coeffs, n, i, s, t);
+            if (QUAL && (t1 & (SJ_RESCALE | T1_PENDING))) {
+                const QualOut q = quality_slow(ld, i, sj, t1);
+                sj = q.sj;
+                t1 = (uint8_t)q.t1;
+            }
         }
     }
     uint8_t f;
@@ -503,7 +556,7 @@ __global__ void __launch_bounds__(P1_THREADS, 2) plain_kernel(L ld, int64_t n, B
     if (i < n) {
         double X[24];
         ld.load_stream(i, X);
-        st = body.hex(ld, X, i);
+        st = body.template hex<L, false>(ld, X, i);
     }
     body.epilogue(st, i);
     body.finish();
@@ -690,9 +743,10 @@ struct Pass1Body {                                           // K1/K2: S1-S8 + K
     double* sj;
     uint8_t* t1;
     P1Counts cnt;
-    template <class L>
+    // FAST_RANGE: see pass1_hex; plain_kernel (128 registers) keeps the up-front range test
+    template <class L, bool FAST_RANGE = true>
     __device__ __forceinline__ int hex(const L& ld, const double* X, int64_t i) {
-        return pass1_hex<COEFFS, L, QUAL>(ld, X, i, n, flags, coeffs, sj, t1);
+        return pass1_hex<COEFFS, L, QUAL, FAST_RANGE>(ld, X, i, n, flags, coeffs, sj, t1);
     }
     __device__ __forceinline__ void epilogue(int st, int64_t i) {
         warp_epilogue<false>(st, i, ctl, qsub, qexact, stats);
@@ -822,7 +876,7 @@ __global__ void __launch_bounds__(BK_THREADS, 2)
             bk_issue(coords, n, t + 2 * G, bk_buf + b * BK_STAGE, &full[b], lane);
         }
         const int64_t i = (int64_t)t * BK_THREADS + tid;
-        const int st = body.hex(SoaLoader{coords, n}, X, i);
+        const int st = body.template hex<SoaLoader, false>(SoaLoader{coords, n}, X, i);
         body.epilogue(st, i);
     }
     // ragged tail: the block that would own tile `tiles` does the last n mod 256 hexes with plain loads
@@ -833,7 +887,7 @@ __global__ void __launch_bounds__(BK_THREADS, 2)
             double X[24];
 #pragma unroll
             for (int p = 0; p < 24; ++p) X[p] = __ldcs(coords + (int64_t)p * n + i);
-            st = body.hex(SoaLoader{coords, n}, X, i);
+            st = body.template hex<SoaLoader, false>(SoaLoader{coords, n}, X, i);
         }
         body.epilogue(st, i);
     }
@@ -1653,7 +1707,7 @@ struct BoundsRootBody {
     uint8_t* status;
     unsigned* qcount;
     uint32_t* q;
-    template <class L>
+    template <class L, bool = true>
     __device__ __forceinline__ int hex(const L&, const double* X, int64_t i) {
         double lo, up;
         uint8_t st = 0;

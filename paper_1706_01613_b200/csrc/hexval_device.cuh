@@ -93,6 +93,8 @@ struct Samples {
     double c[8];
     double d[12];
     int ekey;        // abskey of max |edge component|
+    int range_key = 0;     // in: max abskey of node 1's coordinates (0 if the caller tests the range itself)
+    bool suspect = false;  // out: max(ekey, range_key) >= 2^297 -- the hex may be NONFINITE (hexval.cu, out_of_range)
 };
 
 struct NoCornerHook {
@@ -116,6 +118,7 @@ __device__ __forceinline__ void samples20(const double* X, Samples& s, CornerHoo
                               v15.x, v15.y, v15.z, v26.x, v26.y, v26.z, v48.x, v48.y, v48.z, v37.x, v37.y, v37.z};
     const int e = max_abskey<36>(comps);
     s.ekey = e;
+    s.suspect = max(e, s.range_key) >= 0x52800000;        // 2^297 (decided here, before the determinants)
 
     // corners: det(d_xi x, d_eta x, d_zeta x) with the 3 edges at the corner
     s.c[0] = det3(v12, v14, v15);

@@ -733,6 +733,53 @@ def test_test1_is_necessary_at_full_size(cfg):
     assert bool((sj[valid] > 0).all().item())
 
 
+def test_fused_screen_range_decision():
+    """The fused screening pass takes NONFINITE from the edge-scale key (3 masked keys on the
+    fast path, the exact test out of line): NaN / Inf / 2^301 coordinates, in-range hexes at
+    2^298 .. 2^300 (suspects that must still be validated), a huge offset with unit edges (edge
+    key small, node-1 key large) and one beyond the range (edges 0 in fp64), all equal to the
+    plain validity call and, where defined, to the oracle."""
+    U = pins.KAPPA.astype(float)
+    X = np.stack([U.copy() for _ in range(11)])
+    X[0, 3, 1] = np.nan
+    X[1, 0, 0] = np.inf
+    X[2, 7, 2] = -np.inf
+    X[3, 5, 0] = 2.0 ** 301
+    X[4] *= 2.0 ** 299
+    X[5] *= 2.0 ** 298
+    X[6] *= 2.0 ** 296
+    X[7] = (U - 0.5) * 2.0 ** 300                       # |x| = 2^299: in range, edges 2^300
+    X[8] = U + 2.0 ** 40                                # large offset, unit edges
+    X[9] = U * 2.0 ** 250 + 2.0 ** 301                  # out of range through the offset alone
+    X[10, 6, 2] = -(2.0 ** 300) * (1 + 2.0 ** -52)      # just beyond 2^300
+    reps = 40                                            # several warps, mixed with ordinary hexes
+    coords = np.concatenate([hexgen.nodes_to_soa(X), hexgen.ragged_soa(700, seed=77, amp=0.4)] * reps, axis=1)
+    dev = torch.from_numpy(np.ascontiguousarray(coords)).cuda()
+    f, sj, t1 = hv.check_screen_soa(dev)
+    f0, _ = hv.check_soa(dev)
+    sj0, t10 = hv.corner_quality_soa(dev)
+    torch.cuda.synchronize()
+    f, f0 = f.cpu().numpy(), f0.cpu().numpy()
+    assert np.array_equal(f, f0)
+    assert f[:11].tolist() == [3, 3, 3, 3, 1, 1, 1, 1, 1, 3, 3]
+    a, b = sj.cpu().numpy(), sj0.cpu().numpy()
+    assert np.array_equal(np.isnan(a), np.isnan(b)) and np.array_equal(a[~np.isnan(a)], b[~np.isnan(b)])
+    assert np.array_equal(t1.cpu().numpy(), t10.cpu().numpy())
+    assert np.all(np.isnan(a[:4])) and np.all(t1.cpu().numpy()[:4] == 0) and np.all(np.isnan(a[9:11]))
+    assert np.allclose(a[4:8], 1.0, rtol=1e-13, atol=0) and np.all(t1.cpu().numpy()[4:8] == 1)
+    ref = oracle.check_soa(coords)
+    assert_flags_match(f, ref, allow_near=True)
+    # the indexed path: the same 11 hexes as 88 vertices
+    verts = np.ascontiguousarray(X.reshape(-1, 3))
+    idx = np.arange(88, dtype=np.int32).reshape(11, 8)
+    fi, sji, t1i = hv.check_screen_indexed(torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda())
+    torch.cuda.synchronize()
+    assert fi.cpu().numpy().tolist() == f[:11].tolist()
+    ai = sji.cpu().numpy()
+    assert np.array_equal(np.isnan(ai), np.isnan(a[:11])) and np.array_equal(ai[~np.isnan(ai)], a[:11][~np.isnan(a[:11])])
+    assert np.array_equal(t1i.cpu().numpy(), t1.cpu().numpy()[:11])
+
+
 def test_fused_screen_indexed_config3_slice():
     verts, idx = hexgen.indexed_config(3, start=4242, count=256 * 148 + 555)
     v, i = torch.from_numpy(verts).cuda(), torch.from_numpy(idx).cuda()
