@@ -53,13 +53,20 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
 DEBUG_LIB = os.path.join(HERE, "libhexval_debug.so")
 
 
+# invariant traps + the smallest practical K4 stack capacity: the capacity-adaptive pop size runs in
+# its one-node mode on inputs the default capacity never throttles (tests/test_gpu_parity.py)
+SMALLCAP_LIB = os.path.join(HERE, "libhexval_smallcap.so")
+
+
 def build_all(force: bool = False) -> list[str]:
-    """The product library and its HEXVAL_DEBUG variant (invariant traps; used by the GPU tests)."""
+    """The product library and its test variants (used by the GPU tests): HEXVAL_DEBUG invariant
+    traps, and the same with a 416-slot K4 stack."""
     out = [build(force=force)]
-    if force or not os.path.exists(DEBUG_LIB) or any(os.path.getmtime(d) > os.path.getmtime(DEBUG_LIB) for d in DEPS):
-        out.append(build(out=DEBUG_LIB, defines=("HEXVAL_DEBUG",)))
-    else:
-        out.append(DEBUG_LIB)
+    for lib, defines in ((DEBUG_LIB, ("HEXVAL_DEBUG",)), (SMALLCAP_LIB, ("HEXVAL_DEBUG", "HEXVAL_K4_CAP=416"))):
+        if force or not os.path.exists(lib) or any(os.path.getmtime(d) > os.path.getmtime(lib) for d in DEPS):
+            out.append(build(out=lib, defines=defines))
+        else:
+            out.append(lib)
     return out
 
 

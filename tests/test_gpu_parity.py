@@ -1091,6 +1091,34 @@ def test_debug_build_invariants(tmp_path):
     assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
 
 
+def test_small_stack_capacity_gives_the_same_results(tmp_path):
+    """K4's capacity-adaptive pop size (hexval.cu "Stack capacity"): a build with 416 stack
+    slots per warp (and the invariant traps on) throttles its pops down to the one-node
+    depth-first mode on config-4 trees, wide random Bezier trees and the NEXT-1 bounds --
+    verdicts, SUBDIVIDED bits, depth-cap outcomes and bounds must equal the default build's."""
+    import subprocess
+    import sys
+    from paper_1706_01613_b200 import build as hvbuild
+    if not os.path.exists(hvbuild.SMALLCAP_LIB):
+        pytest.skip("libhexval_smallcap.so not built")
+    root = hexgen.__file__.rsplit("/", 2)[0]
+    sys.path.insert(0, os.path.join(root, "tools"))
+    import smallcap_check
+    ours = smallcap_check.run()
+    out = str(tmp_path / "smallcap.npz")
+    env = dict(os.environ, HEXVAL_LIB="libhexval_smallcap.so")
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "smallcap_check.py"), out], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.startswith("ok libhexval_smallcap.so"), r.stdout + r.stderr
+    small = np.load(out)
+    for key in ("f4", "fb", "s", "n_valid", "n_invalid", "n_undetermined"):
+        assert np.array_equal(ours[key], small[key]), key
+    for key in ("lo", "up"):
+        assert np.array_equal(ours[key], small[key], equal_nan=True), key
+    assert int((ours["f4"] & hv.FLAG_SUBDIVIDED != 0).sum()) > 5000          # K4 really ran
+    assert len(set((ours["fb"] & 3).tolist())) >= 2                          # mixed verdicts on the Bezier trees
+
+
 # --------------------------------------------------------------------------
 # large sizes: 64-bit plane offsets (p * n * 8 > 2^32) and long queues
 # --------------------------------------------------------------------------
