@@ -1113,8 +1113,16 @@ def test_small_stack_capacity_gives_the_same_results(tmp_path):
     small = np.load(out)
     for key in ("f4", "fb", "s", "n_valid", "n_invalid", "n_undetermined"):
         assert np.array_equal(ours[key], small[key]), key
-    for key in ("lo", "up"):
-        assert np.array_equal(ours[key], small[key], equal_nan=True), key
+    # the NEXT-1 bounds depend on the traversal order (a node is split iff its minimum is below the
+    # upper bound *found so far* minus tol), so the two builds' certified intervals may differ --
+    # but both contain min det J: they overlap, and their ends differ by at most the wider width
+    lo_a, up_a, lo_b, up_b = ours["lo"], ours["up"], small["lo"], small["up"]
+    assert np.array_equal(np.isnan(lo_a), np.isnan(lo_b)) and not np.isnan(lo_a).any()
+    width = np.maximum(up_a - lo_a, up_b - lo_b)
+    assert np.all(lo_a <= up_a) and np.all(lo_b <= up_b)
+    assert np.all(np.maximum(lo_a, lo_b) <= np.minimum(up_a, up_b))
+    assert np.all(np.abs(lo_a - lo_b) <= width) and np.all(np.abs(up_a - up_b) <= width)
+    assert float(np.mean(lo_a == lo_b)) > 0.5                                # mostly the same trees
     assert int((ours["f4"] & hv.FLAG_SUBDIVIDED != 0).sum()) > 5000          # K4 really ran
     assert len(set((ours["fb"] & 3).tolist())) >= 2                          # mixed verdicts on the Bezier trees
 
