@@ -1124,7 +1124,7 @@ def test_small_stack_capacity_gives_the_same_results(tmp_path):
     assert np.all(np.abs(lo_a - lo_b) <= width) and np.all(np.abs(up_a - up_b) <= width)
     assert float(np.mean(lo_a == lo_b)) > 0.5                                # mostly the same trees
     assert int((ours["f4"] & hv.FLAG_SUBDIVIDED != 0).sum()) > 5000          # K4 really ran
-    assert len(set((ours["fb"] & 3).tolist())) >= 2                          # mixed verdicts on the Bezier trees
+    assert set((ours["fb"] & 3).tolist()) >= {hv.INVALID, hv.VALID, hv.UNDETERMINED}   # all verdicts on the Bezier trees
 
 
 # --------------------------------------------------------------------------

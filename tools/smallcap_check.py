@@ -11,6 +11,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import hexgen  # noqa: E402
+from tests import pins  # noqa: E402  (Fig. 3 index table)
 import paper_1706_01613_b200 as hv  # noqa: E402
 
 
@@ -20,11 +21,21 @@ def run():
     st = hv.Stats()
     f4, _ = hv.check_soa(d4, stats=st)
     lo, up, s = hv.min_detj_bounds_soa(d4[:, :4001].contiguous(), 1e-3)
-    g = torch.Generator(device="cuda").manual_seed(5)
-    B = torch.rand(27, 2001, dtype=torch.float64, device="cuda", generator=g) - 0.02   # deep, wide trees
-    B[:8] = B[:8].abs() + 1e-3                                                         # corners positive
+    # Bezier trees (the recipe of test_classify_bezier_depth_cap_and_random): functions with one
+    # interior zero (depth cap -> UNDETERMINED), lifted copies (deep VALID trees), random
+    # coefficients with negative dips (INVALID / VALID after subdivision)
+    rng = np.random.default_rng(15)
+    cols = []
+    for a in (1.0 / 3.0, 0.3, 0.7, 0.45):
+        q = np.array([a * a, a * (a - 1.0), (1.0 - a) ** 2])
+        pz = np.array([q[i] + q[j] + q[k] for i, j, k in pins.XI2])          # Fig. 3 coefficient order
+        cols += [pz, pz + 1e-3, pz + 1e-5]
+    for _ in range(2000):
+        b = rng.uniform(0.05, 1.0, size=27)
+        b[rng.integers(0, 27, size=rng.integers(1, 4))] -= rng.uniform(0.0, 1.5)
+        cols.append(b)
+    B = torch.from_numpy(np.array(cols).T.copy()).cuda()
     fb = hv.classify_bezier(B)
-    fb = fb[0] if isinstance(fb, tuple) else fb
     torch.cuda.synchronize()
     stats = st.read()
     return {"f4": f4.cpu().numpy(), "lo": lo.cpu().numpy(), "up": up.cpu().numpy(), "s": s.cpu().numpy(),
