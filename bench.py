@@ -43,6 +43,8 @@ FP64_OPS_PER_NODE = 294
 # products, 19 Step-2 compares, ~90 for T~, 18 Step-4 compares)
 FP64_OPS_PER_HEX = 381
 FP64_PEAK_GOPS = 148 * 64 * 1.965            # datasheet-level fallback when the probe cannot run
+K4_L1_BYTES_PER_NODE = 2 * 224               # K4's stack round trip: 7 x 32 B pushed + 7 x 32 B popped per node
+K4_L1_PEAK_GBS = 148 * 64 * 1.965            # L1 data pipe at 64 B/clk/SM for 256-bit accesses (ncu, K4)
 CONFIG_DESC = {
     0: "config0: 10k perturbed unit cubes, SoA fp64, noise U[-0.25,0.25]^3, seed 0",
     1: "config1: 10M perturbed unit cubes, SoA fp64, noise U[-0.35,0.35]^3, seed 1",
@@ -675,6 +677,15 @@ def run_secondary(args):
         "fp64_ops_per_node": FP64_OPS_PER_NODE,
         "fp64_achieved": st["n_nodes"] * FP64_OPS_PER_NODE / k4_s,
         "frac": st["n_nodes"] * FP64_OPS_PER_NODE / k4_s / peak,
+        # the kernel's second roofline (K4): a node is written to the warp's stack
+        # once and read back once, 2 x 224 B through the L1 data pipe, which moves these 256-bit
+        # accesses at 64 B/clk/SM (ncu: l1tex__data_pipe_lsu_wavefronts 50.0% at 2 x 1.16 TB per call,
+        # profiles/r02/s4/subdiv_c4_l1_metrics.txt); the peak is derived from that rate at 1965 MHz
+        "lsu_roofline": {"bound": "l1 data pipe", "bytes_per_node": K4_L1_BYTES_PER_NODE,
+                         "achieved": st["n_nodes"] * K4_L1_BYTES_PER_NODE / k4_s / 1e9,
+                         "peak": K4_L1_PEAK_GBS, "unit": "GB/s",
+                         "frac": st["n_nodes"] * K4_L1_BYTES_PER_NODE / k4_s / 1e9 / K4_L1_PEAK_GBS,
+                         "peak_source": "derived: 148 SMs x 64 B/clk x 1.965 GHz (rate measured with ncu)"},
         "timing": f"mean CUPTI kernel duration over {ksteps} calls"}
     del c4, fl4
     torch.cuda.empty_cache()
