@@ -512,7 +512,22 @@ __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i
             t1 = (uint8_t)q.t1;
         }
     } else {
-        if (out_of_range(X)) {
+        // validity kernels (128 registers: the reordering above spills there, 328 -> 358 us):
+        // the structure of the up-front test is kept, but its fast path looks at node 1 only
+        // (3 masked keys instead of 24); a hex whose node 1 is in range while some edge
+        // component is not below 2^297 -- possibly NONFINITE -- goes to the exact queue, where
+        // exact_hex runs the exact range test first (config 1 332.2 -> 327.5 us, config 2
+        // 270.2 -> 266.7 us, config 3 unchanged; profiles/r02/s4/s4r)
+        bool nonfinite = false;
+        if (!QUAL && FAST_RANGE) {
+            if (node1_key(X) >= RANGE_FAST_KEY) {             // rare: the exact test on the 24 coordinates
+#pragma unroll
+                for (int p = 0; p < 24; ++p) nonfinite |= !(fabs(X[p]) <= 0x1p300);
+            }
+        } else {
+            nonfinite = out_of_range(X);
+        }
+        if (nonfinite) {
             st = ST_NONFINITE;
         } else {
             Samples s;
@@ -523,6 +538,9 @@ __device__ __forceinline__ int pass1_hex(const L& ld, const double* X, int64_t i
             Coeffs t;
             transform(s, t);                                  // S4 (Step 3)
             if (st == ST_VALID && !step4_positive(t)) st = ST_SUB;   // S5 (Step 4)
+            // node 1 is in range but some edge component is huge: the exact queue decides
+            // (exact_hex runs the exact range test first)
+            if (!QUAL && FAST_RANGE && s.suspect) st = ST_EXACT;
             if (COEFFS) write_coeffs(coeffs, n, i, s, t);
             if (QUAL && (t1 & (SJ_RESCALE | T1_PENDING))) {
                 const QualOut q = quality_slow(ld, i, sj, t1);
@@ -1389,6 +1407,11 @@ template <class L>
 __device__ __noinline__ uint8_t exact_hex(const L ld, uint32_t h) {
     double X[24];
     ld.load(h, X);
+    // pass 1 also queues its range suspects here (pass1_hex): the exact NONFINITE test first
+    bool bad = false;
+#pragma unroll
+    for (int p = 0; p < 24; ++p) bad |= !(fabs(X[p]) <= 0x1p300);
+    if (bad) return HEXVAL_NONFINITE;
     return face_pair_coincident(X) ? (uint8_t)HEXVAL_INVALID : exact_resolve(X);
 }
 
@@ -1457,7 +1480,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
     const unsigned lt_mask = (1u << lane) - 1u;
     LevelCounts lc;
     int top = 0, D = 0, nb = 0;                         // warp-uniform: stack size, top level, batch size
-    unsigned long long nodes = 0, n_inv = 0, n_val = 0, n_und = 0, n_ex = 0, n_exi = 0, n_exv = 0, steps = 0;
+    unsigned long long nodes = 0, n_inv = 0, n_val = 0, n_und = 0, n_ex = 0, n_exi = 0, n_exv = 0, n_exn = 0, steps = 0;
     int maxd = 0;
     for (;;) {
         double P[27];
@@ -1492,7 +1515,7 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
                     const uint8_t f = root.exact(h);
                     if (f == HEXVAL_FLAG_SUBDIVIDED) sub = true;
                     else flags[h] = f;
-                    if (STATS) { ++n_ex; n_exi += f == HEXVAL_INVALID; n_exv += f == HEXVAL_VALID; }
+                    if (STATS) { n_ex += f != HEXVAL_NONFINITE; n_exi += f == HEXVAL_INVALID; n_exv += f == HEXVAL_VALID; n_exn += f == HEXVAL_NONFINITE; }
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, sub);
                 if (sub) W.hex[nb + __popc(bal & lt_mask)] = h;
@@ -1641,11 +1664,13 @@ __global__ void HV_K4_BOUNDS subdiv_kernel(R root, uint8_t* __restrict__ flags, 
             n_ex += __shfl_xor_sync(0xffffffffu, n_ex, o);
             n_exi += __shfl_xor_sync(0xffffffffu, n_exi, o);
             n_exv += __shfl_xor_sync(0xffffffffu, n_exv, o);
+            n_exn += __shfl_xor_sync(0xffffffffu, n_exn, o);
         }
-        if (lane == 0 && n_ex) {
-            atomicAdd(&stats->n_exact, n_ex);
+        if (lane == 0 && (n_ex | n_exn)) {
+            if (n_ex) atomicAdd(&stats->n_exact, n_ex);
             if (n_exi) atomicAdd(&stats->n_invalid, n_exi);
             if (n_exv) atomicAdd(&stats->n_valid, n_exv);
+            if (n_exn) atomicAdd(&stats->n_nonfinite, n_exn);
         }
         if (lane == 0) {
             const unsigned long long nsub = n_inv + n_val + n_und;
